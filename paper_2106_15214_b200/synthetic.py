@@ -1,0 +1,140 @@
+"""Seeded synthetic stand-ins for the five BASELINE.json configurations.
+
+The paper's datasets (Olivetti, a spectrogram, TasteProfile, Moffett AVIRIS;
+PAPER.md:853-1058) are not available, so each BASELINE.json config is
+generated here with the shapes, ranks and value distributions it names.
+Every generator is a pure function of ``(shape, seed)``; wide matrices are
+produced in fixed column chunks with per-chunk seeds, so any column prefix of a
+config is bitwise identical to the prefix of the full matrix (the oracle runs
+on such prefixes).
+
+``uniform_init`` is the "W and H initialised Uniform(0,1) from a seed" rule of
+the configs; the reference itself draws half-normal factors
+(solver.py:137-153, reproduced by :func:`paper_2106_15214_b200.init_factors`).
+"""
+
+from __future__ import annotations
+
+import concurrent.futures as _cf
+import os
+
+import numpy as np
+
+CHUNK = 1 << 16
+
+#: name -> (F, N, K, beta, dtype, iterations) exactly as BASELINE.json states
+CONFIGS = {
+    1: dict(F=361, N=2429, K=49, beta=1.0, dtype="fp64", iters=200),
+    2: dict(F=1024, N=8192, K=32, beta=2.0, dtype="fp32", iters=500),
+    3: dict(F=1025, N=16384, K=20, beta=0.0, dtype="fp32", iters=300),
+    4: dict(F=256, N=4194304, K=12, beta=1.5, dtype="fp32", iters=100),
+    5: dict(F=1000000, N=200000, K=64, beta=1.0, dtype="fp32", iters=100,
+            density=5e-4),
+}
+
+
+def uniform_init(F, N, K, seed):
+    """W (F x K) then H (K x N) ~ Uniform(0,1), exact zeros redrawn."""
+    rng = np.random.default_rng(seed)
+
+    def draw(shape):
+        m = rng.random(shape)
+        while (m == 0.0).any():
+            z = m == 0.0
+            m[z] = rng.random(int(z.sum()))
+        return m
+
+    w = draw((F, K))
+    return w, draw((K, N))
+
+
+def config1(F=361, N=2429, K=49, seed=1):
+    """Dense KL: V = W0 H0 + |N(0, 0.01)|, W0, H0 ~ Gamma(1,1), clip >= 1e-9."""
+    rng = np.random.default_rng(seed)
+    w0 = rng.gamma(1.0, 1.0, size=(F, K))
+    h0 = rng.gamma(1.0, 1.0, size=(K, N))
+    v = w0 @ h0 + np.abs(rng.normal(0.0, 0.01, size=(F, N)))
+    return np.maximum(v, 1e-9)
+
+
+def config2(F=1024, N=8192, K=32, seed=2):
+    """Quadratic loss: exact rank-K V = W0 H0, W0, H0 ~ U(0,1)."""
+    rng = np.random.default_rng(seed)
+    w0 = rng.random((F, K))
+    h0 = rng.random((K, N))
+    return w0 @ h0
+
+
+def config3(F=1025, N=16384, K=20, seed=3):
+    """Itakura-Saito: V = (W0 H0) * E, W0 ~ Gamma(0.5,1) / f, H0 ~ Gamma(0.5,1),
+    E ~ Exponential(1) (a spectrogram-like stand-in)."""
+    rng = np.random.default_rng(seed)
+    w0 = rng.gamma(0.5, 1.0, size=(F, K)) / np.arange(1, F + 1, dtype=float)[:, None]
+    h0 = rng.gamma(0.5, 1.0, size=(K, N))
+    e = rng.exponential(1.0, size=(F, N))
+    return (w0 @ h0) * e
+
+
+def _config4_chunk(endm, seed, c, n, dtype):
+    rng = np.random.default_rng([seed, c])
+    mix = rng.dirichlet(np.full(endm.shape[1], 0.3), size=n).T  # K x n
+    noise = np.abs(rng.normal(0.0, 0.005, size=(endm.shape[0], n)))
+    return (endm @ mix + noise).astype(dtype)
+
+
+def config4(F=256, N=4194304, K=12, seed=4, dtype=np.float64, threads=None):
+    """beta=1.5 hyperspectral stand-in: columns are Dirichlet(0.3) mixtures of K
+    Uniform(0,1) endmember spectra plus |N(0, 0.005)| noise.
+    Generated in 65536-column chunks so every prefix is stable."""
+    endm = np.random.default_rng([seed, 0xE0D]).random((F, K))
+    out = np.empty((F, N), dtype=dtype)
+    nchunks = (N + CHUNK - 1) // CHUNK
+
+    def work(c):
+        lo = c * CHUNK
+        hi = min(N, lo + CHUNK)
+        out[:, lo:hi] = _config4_chunk(endm, seed, c, hi - lo, dtype)
+
+    threads = threads or min(8, os.cpu_count() or 1)
+    if nchunks == 1 or threads == 1:
+        for c in range(nchunks):
+            work(c)
+    else:
+        with _cf.ThreadPoolExecutor(threads) as ex:
+            list(ex.map(work, range(nchunks)))
+    return out
+
+
+def config5(F=1000000, N=200000, density=5e-4, seed=5, alpha=1.1):
+    """Sparse counts (CSR): per-row nonzero counts ~ Poisson(density*N), column
+    ids ~ Zipf(alpha) popularity over a seeded column permutation (duplicates
+    within a row merged; one extra entry per row and per column so no row or
+    column is empty), values Geometric(0.3)+1 stored as fp32.
+
+    Returns (indptr int64, indices int32, data float32, (F, N))."""
+    rng = np.random.default_rng(seed)
+    ranks = np.arange(1, N + 1, dtype=float)
+    p = ranks ** (-alpha)
+    cdf = np.cumsum(p / p.sum())
+    perm = rng.permutation(N).astype(np.int32)
+    counts = rng.poisson(density * N, size=F)
+    total = int(counts.sum())
+    cols = perm[np.minimum(np.searchsorted(cdf, rng.random(total)), N - 1)]
+    rows = np.repeat(np.arange(F, dtype=np.int64), counts)
+    # every row and every column gets at least one count: an all-zero row or
+    # column of V drives its factor row/column to exactly 0 under MU, which the
+    # reference rejects (majorizer.py:50-51)
+    fill_r = np.arange(F, dtype=np.int64)
+    fill_c = perm[fill_r % N]
+    extra_c = np.arange(N, dtype=np.int32)
+    extra_r = rng.integers(0, F, size=N)
+    rows = np.concatenate([rows, fill_r, extra_r])
+    cols = np.concatenate([cols, fill_c, extra_c])
+    key = rows * N + cols
+    key = np.unique(key)
+    rows = key // N
+    cols = (key % N).astype(np.int32)
+    vals = (rng.geometric(0.3, size=key.size) + 1).astype(np.float32)
+    indptr = np.zeros(F + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=F), out=indptr[1:])
+    return indptr, cols, vals, (F, N)

@@ -1,0 +1,118 @@
+/*
+ * bnmf.h -- C ABI of the B200-native beta-NMF iteration library (libbnmf.so).
+ *
+ * The reference (betanmf, arXiv 2106.15214) is a pure-Python package with no
+ * FFI of its own; its hot path is the solver loop
+ *     fit / run_jmm / run_bmm(data, config)      solver.py:224-289
+ *     _outer_loop (init, step, objective, stop)  solver.py:292-326
+ *     step: anchor + joint bases + updates       solver.py:239-280, majorizer.py:53-62,
+ *                                                updates.py:157-235, 281-331
+ * Each entry point below names the reference interface it replaces.  A ctypes
+ * binding (paper_2106_15214_b200/_native.py) is what the
+ * reference's fit() would call instead of its numpy loop.
+ *
+ * Conventions: plain pointers and sizes, no torch types.  Every function
+ * returns 0 on success or a negative BNMF_E* code; bnmf_last_error() gives
+ * the message.  All device work is enqueued on the context's own stream;
+ * results are bitwise reproducible for a fixed device count.
+ */
+#ifndef BNMF_H_
+#define BNMF_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BNMF_ABI_VERSION 1
+
+enum { BNMF_FP64 = 0, BNMF_FP32 = 1 };
+enum { BNMF_JMM = 0, BNMF_BMM = 1 };
+/* schedule: 0 = auto, 1 = reference order (SIMT, any L), 2 = fused single-read
+ * pipelined pass (fp32, L = 1, tensor cores) */
+enum { BNMF_SCHED_AUTO = 0, BNMF_SCHED_REFERENCE = 1, BNMF_SCHED_FUSED = 2 };
+
+enum {
+  BNMF_OK = 0,
+  BNMF_E_ARG = -1,
+  BNMF_E_CUDA = -2,
+  BNMF_E_NCCL = -3,
+  BNMF_E_STATE = -4,
+  BNMF_E_UNSUPPORTED = -5
+};
+
+/* Mirrors SolverConfig (solver.py:62-114) after resolution of kappa and gamma. */
+typedef struct bnmf_params {
+  int algorithm;        /* BNMF_JMM / BNMF_BMM            (config.algorithm)   */
+  int sub_iters;        /* L for JMM                      (config.sub_iters)   */
+  int sub_iters_w;      /* L_W for BMM (0 -> sub_iters)   (config.sub_iters_w) */
+  int sub_iters_h;      /* L_H for BMM (0 -> sub_iters)   (config.sub_iters_h) */
+  double beta;          /* config.beta                                          */
+  double gamma;         /* config.gamma (solver.py:107-109)                     */
+  double kappa;         /* resolved shift (solver.py:205-221)                   */
+  double floor;         /* config.denominator_floor                             */
+  double tol;           /* config.tol (solver.py:174-180)                       */
+  int compute_kkt;      /* per-iteration KKT residuals (solver.py:313)          */
+  int schedule;         /* BNMF_SCHED_*                                         */
+} bnmf_params;
+
+typedef struct bnmf_ctx bnmf_ctx;
+
+int bnmf_abi_version(void);
+int bnmf_device_count(int* count);
+
+/* Context on CUDA device `device` computing in `dtype` (BNMF_FP64/BNMF_FP32).
+ * Replaces the implicit numpy state of solver._outer_loop. */
+int bnmf_ctx_create(bnmf_ctx** out, int device, int dtype);
+void bnmf_ctx_destroy(bnmf_ctx* ctx);
+const char* bnmf_last_error(const bnmf_ctx* ctx); /* ctx may be NULL */
+
+/* N-column sharding across ranks (one process per GPU).  Rank 0 creates the
+ * 128-byte NCCL unique id, the host layer broadcasts it.  No reference
+ * counterpart (the reference is single-process). */
+int bnmf_nccl_unique_id(void* id128);
+int bnmf_ctx_init_comm(bnmf_ctx* ctx, int rank, int nranks, const void* id128,
+                       int64_t n_global);
+
+/* Data: the local column block V[:, n0:n0+N] (F x N, row stride ld elements),
+ * src_dtype BNMF_FP64/BNMF_FP32, host or device memory.  kappa is added on the
+ * device (DataMatrix.shifted, core.py:216-220). */
+int bnmf_set_dense(bnmf_ctx* ctx, const void* v, int src_dtype, int src_on_device,
+                   int64_t F, int64_t N, int64_t ld, double kappa);
+
+/* Factors: W (F x K) and the local H block (K x N), fp64 row-major host or
+ * device memory (init_factors, solver.py:137-153, or an injected init). */
+int bnmf_set_factors(bnmf_ctx* ctx, const double* w, const double* h, int64_t K,
+                     int src_on_device);
+
+/* Start a fit: validates params, resets the trace (TraceRow list) and the
+ * stop state; max_iters = config.max_outer_iters. */
+int bnmf_begin(bnmf_ctx* ctx, const bnmf_params* p, int64_t max_iters);
+/* Enqueue n outer iterations (solver.py:301-319) asynchronously.  Iterations
+ * after a stop (should_stop) or past max_iters are no-ops on the device. */
+int bnmf_step(bnmf_ctx* ctx, int64_t n);
+/* Same, bracketed by CUDA events on the context stream; *ms = device time. */
+int bnmf_step_timed(bnmf_ctx* ctx, int64_t n, float* ms);
+/* Wait for the stream; report finished iterations and convergence. */
+int bnmf_sync(bnmf_ctx* ctx, int64_t* iters_done, int* converged);
+/* Trace rows 1..n: objective, cumulative loop seconds, kkt (2 per row, may be
+ * NULL).  TraceRow of solver.py:54-59. */
+int bnmf_read_trace(bnmf_ctx* ctx, double* obj, double* seconds, double* kkt, int64_t n);
+/* Normalised factors W (F x K) and local H (K x N), fp64 host. */
+int bnmf_get_factors(bnmf_ctx* ctx, double* w, double* h);
+
+/* Whole fit: begin + steps until stop or max_iters (fit, solver.py:285-289). */
+int bnmf_run(bnmf_ctx* ctx, const bnmf_params* p, int64_t max_iters,
+             int64_t* iters_done, int* converged);
+
+/* Introspection for the bench / tests. */
+int bnmf_launches_per_iter(bnmf_ctx* ctx, int* launches);
+int bnmf_active_schedule(bnmf_ctx* ctx, int* schedule);
+void* bnmf_stream(bnmf_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BNMF_H_ */

@@ -1,0 +1,63 @@
+"""B200-native beta-NMF (joint-MM and block MU) -- drop-in for the solver
+entry points of the reference ``betanmf`` package (arXiv 2106.15214).
+
+    import paper_2106_15214_b200 as betanmf
+    res = betanmf.fit(V, betanmf.SolverConfig(beta=1, rank=49, algorithm="jmm"))
+
+The per-iteration work runs in libbnmf.so (CUDA, sm_100a); there is no CPU
+fallback.  See DESIGN.md and INTEGRATION.md.
+"""
+
+from .core import (
+    DEFAULT_FLOOR,
+    BetaParam,
+    DataMatrix,
+    DivergenceDomainError,
+    FactorPair,
+    beta_divergence,
+    default_kappa,
+    gamma_exponent,
+)
+from .solver import (
+    FitResult,
+    SolverConfig,
+    Termination,
+    TraceRow,
+    fit,
+    get_context,
+    init_factors,
+    normalize,
+    run_bmm,
+    run_jmm,
+    should_stop,
+    synthetic_low_rank,
+)
+from .updates import Algorithm, OpCounter, UpdateKind
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Algorithm",
+    "BetaParam",
+    "DEFAULT_FLOOR",
+    "DataMatrix",
+    "DivergenceDomainError",
+    "FactorPair",
+    "FitResult",
+    "OpCounter",
+    "SolverConfig",
+    "Termination",
+    "TraceRow",
+    "UpdateKind",
+    "beta_divergence",
+    "default_kappa",
+    "fit",
+    "gamma_exponent",
+    "get_context",
+    "init_factors",
+    "normalize",
+    "run_bmm",
+    "run_jmm",
+    "should_stop",
+    "synthetic_low_rank",
+]

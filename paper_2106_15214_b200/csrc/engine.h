@@ -1,0 +1,70 @@
+// Host-side engine interface shared by engine.cu and the fused tensor-core
+// pass (fused_tc.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/bnmf.h"
+#include "bnmf_common.cuh"
+
+namespace bnmf {
+
+struct EngineBase {
+  int device = 0, dtype = 0;
+  std::string err;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm_nccl = nullptr;
+  int rank = 0, nranks = 1;
+  int64_t n_global = 0;
+  int launches_per_iter = 0;
+  int active_schedule = 0;
+  bool fused_active = false;
+
+  virtual ~EngineBase() {}
+  int fail(int code, const std::string& msg);
+  virtual int set_dense(const void* v, int src_dtype, int on_dev, int64_t F, int64_t N,
+                        int64_t ld, double kappa) = 0;
+  virtual int set_factors(const double* w, const double* h, int64_t K, int on_dev) = 0;
+  virtual int get_factors(double* w, double* h) = 0;
+  virtual int begin(const bnmf_params* p, int64_t max_iters) = 0;
+  virtual int step(int64_t n) = 0;
+  virtual int sync(int64_t* done, int* conv) = 0;
+  virtual int read_trace(double* obj, double* sec, double* kkt, int64_t n) = 0;
+  virtual int init_comm(int rank, int nranks, const void* id, int64_t n_global) = 0;
+};
+
+// What the fused fp32 pass needs from the engine (device pointers are owned by
+// the engine; Wt / Ht hold the normalised iterate in the standard layouts:
+// W F x K row-major, H transposed N x K row-major).
+struct FusedIO {
+  int F = 0, N = 0, K = 0;
+  size_t ldv = 0;
+  const float* V = nullptr;
+  float *Wt = nullptr, *Wc = nullptr, *Ht = nullptr, *Hc = nullptr;
+  double* comm = nullptr;   // >= 2*F*K + 8 doubles, reduced / allreduced sums
+  double* norms = nullptr;  // K
+  double *tr_obj = nullptr, *tr_sec = nullptr, *tr_kkt = nullptr;
+  RunState* st = nullptr;
+  cudaStream_t stream = nullptr;
+  Scalars sc{};
+  int algorithm = 0;
+  int compute_kkt = 0;
+  int nranks = 1;
+  ncclComm_t nccl = nullptr;
+  int64_t n_global = 0;
+  int* launches = nullptr;
+};
+
+struct FusedState;
+bool fused_supported(int dtype, int F, int K, int algorithm, int L, int Lw, int Lh, double beta);
+int fused_create(FusedState** out, const FusedIO& io, std::string& err);
+int fused_begin(FusedState* fs, const FusedIO& io, std::string& err);
+int fused_enqueue_iteration(FusedState* fs, const FusedIO& io, int slot, std::string& err);
+int fused_export(FusedState* fs, const FusedIO& io, std::string& err);
+void fused_destroy(FusedState* fs);
+
+}  // namespace bnmf

@@ -1,0 +1,283 @@
+// SIMT kernels of the reference-order schedule (any dtype, any beta, any
+// sub-iteration count).  These follow the reference loop literally:
+//   W-side pass  : updates.py:203-220 (jmm) / 157-170 (bmm)
+//   H-side pass  : updates.py:223-235 (jmm) / 173-181 (bmm)
+//   objective    : solver.py:304-309 + core.py:89-114
+//   KKT          : diagnostics.py:46-59
+// V is F x ldv row-major; W is F x K row-major; H is stored transposed
+// ("Ht", N x K row-major, k contiguous per column n).  All reductions are
+// fixed-order (no float atomics): results are bitwise reproducible.
+#pragma once
+
+#include "bnmf_common.cuh"
+
+namespace bnmf {
+
+constexpr int ST_TF = 32;       // rows of F per tile
+constexpr int ST_NC = 32;       // columns of N per tile
+constexpr int ST_THREADS = 256;
+constexpr int ST_KCH = 64;      // k handled per accumulation sweep (8 per thread)
+constexpr int ST_KMAX = 128;    // largest rank of the SIMT path
+
+enum PassMode : int { PM_UPDATE = 0, PM_KKT = 1 };
+
+__host__ __device__ inline int kstride(int K) { return (K & 1) ? K : K + 1; }
+
+// Cooperative copy of `rows` rows of K values (global row stride K) into a
+// shared buffer with row stride ks; rows past `valid` are zero-filled.
+template <typename T>
+__device__ __forceinline__ void load_rows(T* dst, const T* __restrict__ src, int rows,
+                                          int valid, int K, int ks) {
+  for (int i = threadIdx.x; i < rows * K; i += blockDim.x) {
+    int r = i / K, k = i - r * K;
+    dst[r * ks + k] = r < valid ? src[(size_t)r * K + k] : T(0);
+  }
+}
+
+// Z tile for rows [f0, f0+TF) x cols [n0, n0+NC): y = W[f,:] . H[:,n] + kappa,
+// then (zn, zd) by the beta rule (or the KKT gradient core in zn).  Entries
+// outside the matrix are 0 so they never contribute.
+template <int BC, int MODE, typename T>
+__device__ __forceinline__ void z_tile(const T* __restrict__ V, size_t ldv, int F, int N,
+                                       int f0, int n0, const T* Ws, const T* Hs, int K,
+                                       int ks, T kappa, T beta, T* Zn, T* Zd) {
+  for (int e = threadIdx.x; e < ST_TF * ST_NC; e += blockDim.x) {
+    int f = e / ST_NC, n = e - f * ST_NC;
+    T zn = T(0), zd = T(0);
+    if (f0 + f < F && n0 + n < N) {
+      const T* wr = Ws + f * ks;
+      const T* hr = Hs + n * ks;
+      T y = T(0);
+      for (int k = 0; k < K; ++k) y = fma(wr[k], hr[k], y);
+      y += kappa;
+      T x = V[(size_t)(f0 + f) * ldv + (n0 + n)];
+      if (MODE == PM_KKT) {
+        zn = grad_core<BC, T>(x, y, beta);
+      } else {
+        bases<BC, T>(x, y, beta, zn, zd);
+      }
+    }
+    Zn[f * (ST_NC + 1) + n] = zn;
+    Zd[f * (ST_NC + 1) + n] = zd;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// W-side partial sums over a column segment:
+//   num[f,k] = sum_n Zn[f,n] C1[n,k],  den[f,k] = sum_n Zd[f,n] C2[n,k]
+// part layout: [seg][2][F][K] (double).  Grid (ceil(F/TF), S).
+template <int BC, int MODE, typename T>
+__global__ void __launch_bounds__(ST_THREADS)
+wside_partials(const T* __restrict__ V, size_t ldv, int F, int N, int K,
+               const T* __restrict__ Wp, const T* __restrict__ Hp,
+               const T* __restrict__ C1, const T* __restrict__ C2,
+               int seg_cols, Scalars sc, double* __restrict__ part,
+               const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int ks = kstride(K);
+  T* Ws = reinterpret_cast<T*>(smem_raw);
+  T* Hs = Ws + ST_TF * ks;
+  T* C1s = Hs + ST_NC * ks;
+  T* C2s = C1s + ST_NC * ks;
+  T* Zn = C2s + ST_NC * ks;
+  T* Zd = Zn + ST_TF * (ST_NC + 1);
+
+  const int f0 = blockIdx.x * ST_TF;
+  const int seg = blockIdx.y;
+  const int nbeg = seg * seg_cols;
+  const int nend = min(N, nbeg + seg_cols);
+  const T kappa = T(sc.kappa), beta = T(sc.beta);
+
+  load_rows(Ws, Wp + (size_t)f0 * K, ST_TF, F - f0, K, ks);
+
+  const int fl = threadIdx.x & 31;   // row within the tile
+  const int kg = threadIdx.x >> 5;   // k group (warp-uniform)
+  const int nkc = (K + ST_KCH - 1) / ST_KCH;
+  double accn[ST_KMAX / 8], accd[ST_KMAX / 8];
+#pragma unroll
+  for (int j = 0; j < ST_KMAX / 8; ++j) { accn[j] = 0.0; accd[j] = 0.0; }
+
+  for (int n0 = nbeg; n0 < nend; n0 += ST_NC) {
+    __syncthreads();
+    int valid = min(ST_NC, nend - n0);
+    load_rows(Hs, Hp + (size_t)n0 * K, ST_NC, valid, K, ks);
+    load_rows(C1s, C1 + (size_t)n0 * K, ST_NC, valid, K, ks);
+    if (MODE != PM_KKT) load_rows(C2s, C2 + (size_t)n0 * K, ST_NC, valid, K, ks);
+    __syncthreads();
+    z_tile<BC, MODE, T>(V, ldv, F, nend, f0, n0, Ws, Hs, K, ks, kappa, beta, Zn, Zd);
+    __syncthreads();
+    const T* zr = Zn + fl * (ST_NC + 1);
+    const T* zdr = Zd + fl * (ST_NC + 1);
+#pragma unroll
+    for (int j = 0; j < ST_KMAX / 8; ++j) {
+      int k = kg + 8 * j;
+      if (j < nkc * 8 && k < K) {
+        T sn = T(0), sd = T(0);
+        for (int n = 0; n < ST_NC; ++n) {
+          sn = fma(zr[n], C1s[n * ks + k], sn);
+          if (MODE != PM_KKT) sd = fma(zdr[n], C2s[n * ks + k], sd);
+        }
+        accn[j] += double(sn);
+        accd[j] += double(sd);
+      }
+    }
+  }
+  if (f0 + fl < F) {
+    double* pn = part + ((size_t)seg * 2 + 0) * F * K + (size_t)(f0 + fl) * K;
+    double* pd = part + ((size_t)seg * 2 + 1) * F * K + (size_t)(f0 + fl) * K;
+#pragma unroll
+    for (int j = 0; j < ST_KMAX / 8; ++j) {
+      int k = kg + 8 * j;
+      if (k < K) { pn[k] = accn[j]; pd[k] = accd[j]; }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// H-side pass over a block of NC columns and all F rows.
+//   PM_UPDATE: Hout[n,k] = Hbase[n,k] * (num/max(den,floor))^gamma with
+//              num[k,n] = sum_f C1w[f,k] Zn[f,n], den likewise with C2w/Zd;
+//              den_ones (beta=1): den[k,n] = colsum(C2w)[k] (updates.py:133-137)
+//   PM_KKT   : grad[k,n] = sum_f Wp[f,k] g[f,n]; writes the per-block sum of
+//              |min(Hp[n,k], grad[k,n])| to part[block] (diagnostics.py:56-58)
+template <int BC, int MODE, typename T>
+__global__ void __launch_bounds__(ST_THREADS)
+hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
+           const T* __restrict__ Wp, const T* __restrict__ Hp,
+           const T* __restrict__ C1w, const T* __restrict__ C2w,
+           const T* __restrict__ Hbase, T* __restrict__ Hout,
+           const double* __restrict__ colsum_c2, int den_ones, Scalars sc,
+           double* __restrict__ part, const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int ks = kstride(K);
+  T* Hs = reinterpret_cast<T*>(smem_raw);
+  T* Ws = Hs + ST_NC * ks;
+  T* C1s = Ws + ST_TF * ks;
+  T* C2s = C1s + ST_TF * ks;
+  T* Zn = C2s + ST_TF * ks;
+  T* Zd = Zn + ST_TF * (ST_NC + 1);
+  __shared__ double red[ST_THREADS / 32];
+
+  const int n0 = blockIdx.x * ST_NC;
+  const int valid_n = min(ST_NC, N - n0);
+  const T kappa = T(sc.kappa), beta = T(sc.beta);
+  load_rows(Hs, Hp + (size_t)n0 * K, ST_NC, valid_n, K, ks);
+
+  const int nl = threadIdx.x & 31;
+  const int kg = threadIdx.x >> 5;
+  double accn[ST_KMAX / 8], accd[ST_KMAX / 8];
+#pragma unroll
+  for (int j = 0; j < ST_KMAX / 8; ++j) { accn[j] = 0.0; accd[j] = 0.0; }
+  const bool use_den = (MODE != PM_KKT) && !den_ones;
+
+  for (int f0 = 0; f0 < F; f0 += ST_TF) {
+    __syncthreads();
+    int valid_f = min(ST_TF, F - f0);
+    load_rows(Ws, Wp + (size_t)f0 * K, ST_TF, valid_f, K, ks);
+    if (MODE != PM_KKT) {
+      load_rows(C1s, C1w + (size_t)f0 * K, ST_TF, valid_f, K, ks);
+      if (use_den) load_rows(C2s, C2w + (size_t)f0 * K, ST_TF, valid_f, K, ks);
+    }
+    __syncthreads();
+    z_tile<BC, MODE, T>(V, ldv, F, N, f0, n0, Ws, Hs, K, ks, kappa, beta, Zn, Zd);
+    __syncthreads();
+    const T* A1 = (MODE == PM_KKT) ? Ws : C1s;
+#pragma unroll
+    for (int j = 0; j < ST_KMAX / 8; ++j) {
+      int k = kg + 8 * j;
+      if (k < K) {
+        T sn = T(0), sd = T(0);
+        for (int f = 0; f < ST_TF; ++f) {
+          sn = fma(A1[f * ks + k], Zn[f * (ST_NC + 1) + nl], sn);
+          if (use_den) sd = fma(C2s[f * ks + k], Zd[f * (ST_NC + 1) + nl], sd);
+        }
+        accn[j] += double(sn);
+        accd[j] += double(sd);
+      }
+    }
+  }
+
+  if (MODE == PM_KKT) {
+    double s = 0.0;
+    if (nl < valid_n) {
+#pragma unroll
+      for (int j = 0; j < ST_KMAX / 8; ++j) {
+        int k = kg + 8 * j;
+        if (k < K) s += fabs(fmin(double(Hs[nl * ks + k]), accn[j]));
+      }
+    }
+    // fixed-order block reduction
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < ST_THREADS / 32; ++w) t += red[w];
+      part[blockIdx.x] = t;
+    }
+    return;
+  }
+  if (nl < valid_n) {
+    const double fl = sc.floor;
+    const double g = sc.gamma;
+#pragma unroll
+    for (int j = 0; j < ST_KMAX / 8; ++j) {
+      int k = kg + 8 * j;
+      if (k < K) {
+        double den = den_ones ? colsum_c2[k] : accd[j];
+        double r = accn[j] / fmax(den, fl);
+        double b = double(Hbase[(size_t)(n0 + nl) * K + k]);
+        Hout[(size_t)(n0 + nl) * K + k] = T(b * apply_exponent<double>(r, g));
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Objective partials: sum over tiles of d_beta(V | W H + kappa) in double.
+// Grid (ceil(F/TF), S); part[blockIdx.y * gridDim.x + blockIdx.x].
+template <int BC, typename T>
+__global__ void __launch_bounds__(ST_THREADS)
+objective_partials(const T* __restrict__ V, size_t ldv, int F, int N, int K,
+                   const T* __restrict__ W, const T* __restrict__ Ht, int seg_cols,
+                   Scalars sc, double* __restrict__ part, const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int ks = kstride(K);
+  T* Ws = reinterpret_cast<T*>(smem_raw);
+  T* Hs = Ws + ST_TF * ks;
+  __shared__ double red[ST_THREADS / 32];
+  const int f0 = blockIdx.x * ST_TF;
+  const int nbeg = blockIdx.y * seg_cols;
+  const int nend = min(N, nbeg + seg_cols);
+  const T kappa = T(sc.kappa);
+  load_rows(Ws, W + (size_t)f0 * K, ST_TF, F - f0, K, ks);
+  double s = 0.0;
+  for (int n0 = nbeg; n0 < nend; n0 += ST_NC) {
+    __syncthreads();
+    load_rows(Hs, Ht + (size_t)n0 * K, ST_NC, min(ST_NC, nend - n0), K, ks);
+    __syncthreads();
+    for (int e = threadIdx.x; e < ST_TF * ST_NC; e += blockDim.x) {
+      int f = e / ST_NC, n = e - f * ST_NC;
+      if (f0 + f < F && n0 + n < nend) {
+        T y = T(0);
+        for (int k = 0; k < K; ++k) y = fma(Ws[f * ks + k], Hs[n * ks + k], y);
+        y += kappa;
+        double x = double(V[(size_t)(f0 + f) * ldv + n0 + n]);
+        s += divergence<BC>(x, double(y), sc.beta);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < ST_THREADS / 32; ++w) t += red[w];
+    part[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+}  // namespace bnmf

@@ -1,0 +1,219 @@
+// Small per-iteration kernels: fixed-order reductions of partial sums, the
+// multiplicative factor update, chi maps, normalisation and the trace /
+// stop-rule bookkeeping (solver.py:167-180, 292-326; updates.py:118-123).
+#pragma once
+
+#include "bnmf_common.cuh"
+
+namespace bnmf {
+
+// out[i] = sum_{s < S} part[s * stride + i], fixed order (deterministic).
+__global__ void reduce_segments(const double* __restrict__ part, size_t stride, int S,
+                                size_t count, double* __restrict__ out,
+                                const RunState* st, int slot) {
+  if (st && !iter_active(st, slot)) return;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < S; ++k) s += part[(size_t)k * stride + i];
+    out[i] = s;
+  }
+}
+
+// Single-block fixed-order sum of `count` doubles into *out (count small).
+__global__ void sum_small(const double* __restrict__ in, int count, double* __restrict__ out,
+                          const RunState* st, int slot) {
+  if (st && !iter_active(st, slot)) return;
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) s += in[i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) t += red[w];
+    *out = t;
+  }
+}
+
+// chi1 / chi2 of (M, Mt) entrywise, count entries.
+template <typename T>
+__global__ void chi_maps(const T* __restrict__ M, const T* __restrict__ Mt, T* __restrict__ o1,
+                         T* __restrict__ o2, size_t count, Scalars sc, const RunState* st,
+                         int slot) {
+  if (!iter_active(st, slot)) return;
+  const T beta = T(sc.beta);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x) {
+    T m = M[i], mt = Mt[i];
+    if (o1) o1[i] = chi1<T>(m, mt, beta);
+    if (o2) o2[i] = chi2<T>(m, mt, beta);
+  }
+}
+
+// W-side update: out[f,k] = base[f,k] * (num/max(den,floor))^gamma, where den is
+// either a full F x K array or (den_ones) the row-sum K-vector broadcast.
+template <typename T>
+__global__ void update_w(const T* __restrict__ base, const double* __restrict__ num,
+                         const double* __restrict__ den, int den_is_vec, int F, int K,
+                         T* __restrict__ out, Scalars sc, const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < F * K; i += gridDim.x * blockDim.x) {
+    int k = i % K;
+    double d = den_is_vec ? den[k] : den[i];
+    double r = num[i] / fmax(d, sc.floor);
+    out[i] = T(double(base[i]) * apply_exponent<double>(r, sc.gamma));
+  }
+}
+
+// Column sums of an F x K matrix (K threads, fixed order) -> double K-vector.
+template <typename T>
+__global__ void col_sums(const T* __restrict__ M, int F, int K, double* __restrict__ out,
+                         const RunState* st, int slot) {
+  if (st && !iter_active(st, slot)) return;
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  double s = 0.0;
+  for (int f = 0; f < F; ++f) s += double(M[(size_t)f * K + k]);
+  out[k] = s;
+}
+
+// norms[k] = sqrt(sum_f W[f,k]^2); Wn = W / norms (solver.py:167-171).
+// One warp per column, fixed-order lane partition + shuffle tree.
+template <typename T>
+__global__ void normalize_w(const T* __restrict__ W, int F, int K, T* __restrict__ Wn,
+                            double* __restrict__ norms, const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  int k = blockIdx.x;
+  double s = 0.0;
+  for (int f = threadIdx.x; f < F; f += 32) {
+    double w = double(W[(size_t)f * K + k]);
+    s += w * w;
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  double nrm = sqrt(s);
+  if (threadIdx.x == 0) norms[k] = nrm;
+  for (int f = threadIdx.x; f < F; f += 32)
+    Wn[(size_t)f * K + k] = T(double(W[(size_t)f * K + k]) / nrm);
+}
+
+// Hn[n,k] = H[n,k] * norms[k]  (Ht layout N x K).
+template <typename T>
+__global__ void scale_h(const T* __restrict__ H, size_t N, int K, const double* __restrict__ norms,
+                        T* __restrict__ Hn, const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  size_t count = N * (size_t)K;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x) {
+    int k = int(i % K);
+    Hn[i] = T(double(H[i]) * norms[k]);
+  }
+}
+
+// Mark the start of an iteration (timer, solver.py:302).
+__global__ void begin_iter(RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  st->t_begin = globaltimer();
+}
+
+// Objective bookkeeping + stop rule (solver.py:309-319, 174-180).
+// obj: reduced objective (global, after any allreduce).
+__global__ void finish_iter(RunState* st, int slot, const double* __restrict__ obj,
+                            double* __restrict__ trace_obj, double* __restrict__ trace_sec,
+                            double tol) {
+  if (!iter_active(st, slot)) return;
+  long long it = st->base + slot;
+  double o = *obj;
+  bool stop = false;
+  if (it > 1) {
+    double prev = st->prev_obj;
+    if (o == prev) stop = true;
+    else if (o <= 0.0) stop = false;
+    else stop = (prev - o) / o <= tol;
+  }
+  unsigned long long t = globaltimer();
+  st->elapsed += double(t - st->t_begin) * 1e-9;
+  trace_obj[it - 1] = o;
+  trace_sec[it - 1] = st->elapsed;
+  st->prev_obj = o;
+  st->iters_done = it;
+  if (stop) { st->stop_iter = it; st->converged = 1; }
+}
+
+// res_W = sum |min(W, gradW)| / (F K)   (diagnostics.py:57)
+template <typename T>
+__global__ void kkt_w_residual(const T* __restrict__ W, const double* __restrict__ grad, int F,
+                               int K, const double* __restrict__ resh_sum, size_t KN,
+                               double* __restrict__ trace_kkt, const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < F * K; i += blockDim.x)
+    s += fabs(fmin(double(W[i]), grad[i]));
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) t += red[w];
+    long long it = st->base + slot;
+    trace_kkt[2 * (it - 1) + 0] = t / (double(F) * K);
+    trace_kkt[2 * (it - 1) + 1] = *resh_sum / double(KN);
+  }
+}
+
+__global__ void advance_base(RunState* st, int n) { st->base += n; }
+
+// --- layout conversion helpers (upload / download) -------------------------
+
+// dst[r * ldd + c] = T(src[r * lds + c]) + kappa   (row-major convert)
+template <typename S, typename T>
+__global__ void convert_rows(const S* __restrict__ src, size_t lds, T* __restrict__ dst,
+                             size_t ldd, int rows, size_t cols, double kappa) {
+  size_t count = (size_t)rows * cols;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x) {
+    size_t r = i / cols, c = i - r * cols;
+    double v = double(src[r * lds + c]);
+    dst[r * ldd + c] = kappa != 0.0 ? T(v + kappa) : T(v);
+  }
+}
+
+// K x N (fp64, row-major) -> N x K (T)
+template <typename T>
+__global__ void transpose_in(const double* __restrict__ src, int K, size_t N, T* __restrict__ dst) {
+  size_t count = N * (size_t)K;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x) {
+    size_t n = i / K; int k = int(i - n * K);
+    dst[i] = T(src[(size_t)k * N + n]);
+  }
+}
+
+// N x K (T) -> K x N (fp64)
+template <typename T>
+__global__ void transpose_out(const T* __restrict__ src, int K, size_t N, double* __restrict__ dst) {
+  size_t count = N * (size_t)K;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x) {
+    size_t k = i / N, n = i - k * N;
+    dst[i] = double(src[n * K + k]);
+  }
+}
+
+template <typename T>
+__global__ void to_double(const T* __restrict__ src, size_t count, double* __restrict__ dst) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = double(src[i]);
+}
+
+template <typename T>
+__global__ void from_double(const double* __restrict__ src, size_t count, T* __restrict__ dst) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = T(src[i]);
+}
+
+}  // namespace bnmf

@@ -1,0 +1,133 @@
+"""Parity of the CUDA path (through the drop-in API and the C ABI) against the
+reference, via the golden fixtures it produced (tests/golden/gen_golden.py)
+and the pinned CPU oracle.
+
+Tolerances (BASELINE.json north_star):
+  fp64: W, H and every objective <= 1e-10 relative; KKT <= 1e-6 relative
+  fp32: objective <= 1e-4 relative over the whole trace; trace monotone.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2106_15214_b200 as bn
+from conftest import golden_fit_cases, load_golden, max_rel, parse_cfg
+
+pytestmark = pytest.mark.gpu
+
+FP64_TOL = 1e-10
+
+
+def _fit_case(name, **opts):
+    z = load_golden("fits.npz")
+    cfg = parse_cfg(str(z[f"{name}/cfg"]))
+    config = bn.SolverConfig(**cfg)
+    return z, bn.fit(z[f"{name}/v"], config, **opts)
+
+
+@pytest.mark.parametrize("name", golden_fit_cases())
+def test_fp64_fit_matches_reference(name):
+    z, res = _fit_case(name, schedule="reference")
+    ref_obj = z[f"{name}/obj"]
+    assert res.termination.value == str(z[f"{name}/term"])
+    assert res.iterations == len(ref_obj)
+    obj = np.array([r.objective for r in res.trace])
+    # objectives at round-off level (exact fits) are compared absolutely
+    atol = 1e-14 * float(np.abs(z[f"{name}/v"]).sum())
+    assert np.all(np.abs(obj - ref_obj) <= FP64_TOL * np.abs(ref_obj) + atol)
+    assert max_rel(res.factors.w, z[f"{name}/w"]) <= FP64_TOL
+    assert max_rel(res.factors.h, z[f"{name}/h"]) <= FP64_TOL
+    kkt = np.array([[r.kkt_w, r.kkt_h] for r in res.trace])
+    np.testing.assert_allclose(kkt, z[f"{name}/kkt"], rtol=1e-6, atol=1e-12)
+    assert [r.iteration for r in res.trace] == list(range(1, res.iterations + 1))
+    sec = [r.seconds for r in res.trace]
+    assert all(b >= a for a, b in zip(sec, sec[1:]))
+
+
+def test_config1_full_fp64_jmm_200_iterations():
+    """PR1 gate: config 1 at full size, injected U(0,1) init."""
+    from paper_2106_15214_b200 import synthetic
+    z = load_golden("configs.npz")
+    v = synthetic.config1()
+    assert float(v.sum()) == float(z["cfg1/vsum"])
+    w0, h0 = synthetic.uniform_init(361, 2429, 49, seed=149)
+    for algo in ("jmm", "bmm"):
+        ref_obj = z[f"cfg1_{algo}/obj"]
+        cfg = bn.SolverConfig(beta=1.0, rank=49, algorithm=algo, tol=1e-300,
+                              max_outer_iters=len(ref_obj))
+        res = bn.fit(v, cfg, init=(w0, h0))
+        obj = np.array([r.objective for r in res.trace])
+        assert max_rel(obj, ref_obj) <= FP64_TOL
+        assert max_rel(res.factors.w, z[f"cfg1_{algo}/w"]) <= FP64_TOL
+        assert max_rel(res.factors.h, z[f"cfg1_{algo}/h"]) <= FP64_TOL
+        assert all(b <= a * (1 + 1e-10) for a, b in zip(obj, obj[1:]))
+
+
+CFG = {
+    "cfg2p": (lambda s: s.config2(F=1024, N=1024, K=32), 32, 2.0, None),
+    "cfg3p": (lambda s: s.config3(F=1025, N=1024, K=20), 20, 0.0, None),
+    "cfg4p": (lambda s: s.config4(N=4096), 12, 1.5, 0.0),
+}
+
+
+@pytest.mark.parametrize("schedule", ["reference", "auto"])
+@pytest.mark.parametrize("name", sorted(CFG))
+def test_fp32_configs_objective_within_1e4(name, schedule):
+    from paper_2106_15214_b200 import synthetic
+    z = load_golden("configs.npz")
+    gen, K, beta, kappa = CFG[name]
+    v = gen(synthetic).astype(np.float32)
+    w0, h0 = synthetic.uniform_init(v.shape[0], v.shape[1], K, seed=100 + K)
+    for algo in ("jmm", "bmm"):
+        ref_obj = z[f"{name}_{algo}/obj"]
+        cfg = bn.SolverConfig(beta=beta, rank=K, algorithm=algo, tol=1e-300, kappa=kappa,
+                              max_outer_iters=len(ref_obj))
+        res = bn.fit(v, cfg, init=(w0, h0), dtype="fp32", kkt=False, schedule=schedule)
+        obj = np.array([r.objective for r in res.trace])
+        assert max_rel(obj, ref_obj) <= 1e-4, (algo, max_rel(obj, ref_obj))
+        assert all(b <= a * (1 + 1e-6) for a, b in zip(obj, obj[1:]))
+
+
+def test_bitwise_reproducible():
+    v = bn.synthetic_low_rank(150, 120, 3, noise=0.1, seed=4)
+    for dtype in ("fp64", "fp32"):
+        cfg = bn.SolverConfig(beta=0.0, rank=3, algorithm="jmm", seed=9,
+                              max_outer_iters=30, tol=1e-300)
+        r1 = bn.run_jmm(v, cfg, dtype=dtype)
+        r2 = bn.run_jmm(v, cfg, dtype=dtype)
+        assert np.array_equal(r1.factors.w, r2.factors.w)
+        assert np.array_equal(r1.factors.h, r2.factors.h)
+        assert [t.objective for t in r1.trace] == [t.objective for t in r2.trace]
+
+
+def test_op_counter_semantics():
+    v = bn.synthetic_low_rank(10, 8, 3, noise=0.1, seed=1)
+    counter = bn.OpCounter()
+    cfg = bn.SolverConfig(beta=1.5, rank=3, algorithm="jmm", seed=2, sub_iters=4,
+                          max_outer_iters=5, tol=1e-300)
+    bn.run_jmm(v, cfg, counter=counter)
+    assert counter.anchor_products == 5 and counter.objective_products == 5
+    assert counter.w_updates == 20 and counter.h_updates == 20
+    counter = bn.OpCounter()
+    cfg = bn.SolverConfig(beta=1.5, rank=3, algorithm="bmm", seed=2, sub_iters_w=2,
+                          sub_iters_h=3, max_outer_iters=5, tol=1e-300)
+    bn.run_bmm(v, cfg, counter=counter)
+    assert counter.kernel_products == 25
+
+
+def test_exact_fit_converges_at_second_iteration():
+    init = bn.init_factors(5, 4, 2, seed=3)
+    v = init.w @ init.h
+    for algo in ("bmm", "jmm"):
+        res = bn.fit(v, bn.SolverConfig(beta=2.0, rank=2, algorithm=algo, seed=3))
+        assert res.termination == bn.Termination.CONVERGED
+        assert res.iterations == 2
+
+
+def test_native_library_is_what_ran():
+    """The fit must have gone through libbnmf (no silent fallback)."""
+    ctx = bn.get_context(0, "fp64")
+    v = bn.synthetic_low_rank(20, 16, 2, noise=0.1, seed=5)
+    bn.fit(v, bn.SolverConfig(beta=1.0, rank=2, algorithm="jmm", max_outer_iters=3))
+    assert ctx.launches_per_iter() > 0
+    assert ctx.schedule() in ("reference", "fused")

@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""Benchmark: beta-NMF joint-MM outer iterations/s on B200 (BASELINE.json metric).
+
+Default workload (N=1): BASELINE config 4 -- beta = 1.5 joint-MM, fp32,
+V 256 x 4,194,304 (4.29 GB, far larger than the 126 MB L2), K = 12 -- the
+largest single-GPU configuration and the one the metric's 1-8 GPU scaling is
+quoted on.  A "step" is one outer iteration (solver.py:301-319): update of W and
+H, objective of the new iterate, normalisation.  Under torchrun the columns are
+sharded across ranks (strong scaling of the fixed 4.2M-column problem).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..4]
+    python bench.py --impl reference ...   # CPU reference arm (oracle port)
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "beta-NMF joint-MM outer iterations/s (V-pass HBM GB/s in roofline)"
+
+CONFIGS = {
+    # name: F, N, K, beta, dtype, kappa
+    1: dict(F=361, N=2429, K=49, beta=1.0, dtype="fp64", kappa=0.0),
+    2: dict(F=1024, N=8192, K=32, beta=2.0, dtype="fp32", kappa=0.0),
+    3: dict(F=1025, N=16384, K=20, beta=0.0, dtype="fp32", kappa=None),
+    4: dict(F=256, N=4194304, K=12, beta=1.5, dtype="fp32", kappa=0.0),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
+    ap.add_argument("--algo", default="jmm", choices=["jmm", "bmm"])
+    ap.add_argument("--schedule", default="auto", choices=["auto", "reference", "fused"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def make_data(cfg_id, n0, n1, dtype):
+    from paper_2106_15214_b200 import synthetic as syn
+    c = CONFIGS[cfg_id]
+    npdt = np.float32 if dtype == "fp32" else np.float64
+    if cfg_id == 4:
+        return syn.config4(F=c["F"], N=c["N"], K=c["K"], dtype=npdt, col_range=(n0, n1))
+    gen = {1: syn.config1, 2: syn.config2, 3: syn.config3}[cfg_id]
+    v = gen(F=c["F"], N=c["N"], K=c["K"])
+    return np.ascontiguousarray(v[:, n0:n1]).astype(npdt)
+
+
+def make_init(cfg_id, n0, n1):
+    from paper_2106_15214_b200 import synthetic as syn
+    c = CONFIGS[cfg_id]
+    w0, h0 = syn.uniform_init(c["F"], c["N"], c["K"], seed=100 + c["K"])
+    return w0, np.ascontiguousarray(h0[:, n0:n1])
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops", 1590.0)), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons through NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+        self._stop = threading.Event()
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._loop, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+def cpu_sample(cfg_id, algo, iters=3, n_sample=None):
+    """The oracle (numpy port of the reference loop) on a bounded column prefix,
+    all host cores for BLAS; returns (iterations/s scaled to full N, info)."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import betanmf_oracle as O
+    c = CONFIGS[cfg_id]
+    cores = os.cpu_count() or 1
+    n_sample = n_sample or (min(c["N"], 65536) if cfg_id == 4 else c["N"])
+    v = make_data(cfg_id, 0, n_sample, "fp64" if c["dtype"] == "fp64" else "fp32")
+    v = v.astype(np.float64)
+    w0, h0 = make_init(cfg_id, 0, n_sample)
+    with threadpool_limits(limits=cores):
+        O.run(v, c["beta"], c["K"], algo, kappa=c["kappa"], tol=1e-300, max_outer_iters=1,
+              init=(w0, h0), kkt=False)  # warm
+        t0 = time.perf_counter()
+        O.run(v, c["beta"], c["K"], algo, kappa=c["kappa"], tol=1e-300, max_outer_iters=iters,
+              init=(w0, h0), kkt=False)
+        dt = (time.perf_counter() - t0) / iters
+    scale = c["N"] / n_sample
+    return 1.0 / (dt * scale), dict(cores=cores, n_sample=n_sample, s_per_iter_sample=dt,
+                                   scale=scale)
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    c = CONFIGS[args.config]
+    from threadpoolctl import threadpool_limits
+
+    from oracle import betanmf_oracle as O
+    cores = os.cpu_count() or 1
+    n_sample = min(c["N"], 65536) if args.config == 4 else c["N"]
+    v = make_data(args.config, 0, n_sample, c["dtype"]).astype(np.float64)
+    w0, h0 = make_init(args.config, 0, n_sample)
+    times = []
+    with threadpool_limits(limits=cores):
+        w, h = w0, h0
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            w, h, _, _, _ = O.run(v, c["beta"], c["K"], args.algo, kappa=c["kappa"], tol=1e-300,
+                                  max_outer_iters=1, init=(w, h), kkt=False)
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+    dt = sum(times) / len(times) * (c["N"] / n_sample)
+    val = 1.0 / dt
+    sample = (f"numpy oracle port of the reference loop, fp64, {c['F']}x{n_sample} column prefix "
+              f"(of N={c['N']}), per-iteration time scaled x{c['N'] / n_sample:g}")
+    out = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "iterations/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, world),
+        "cpu_baseline": {"value": val, "unit": "iterations/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": val, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+def workload_config(args, world):
+    c = CONFIGS[args.config]
+    return {"workload": f"config{args.config}: {args.algo} beta={c['beta']} {c['F']}x{c['N']} "
+                        f"K={c['K']} {c['dtype']}",
+            "F": c["F"], "N": c["N"], "K": c["K"], "beta": c["beta"], "algorithm": args.algo,
+            "parallelism": f"N-columns x{world}", "l2": "inputs larger than L2"
+            if c["F"] * c["N"] * (4 if c["dtype"] == "fp32" else 8) > 126e6
+            else "input fits in L2 (no flush; iterations re-read V)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    rank, world, local = dist_env()
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2106_15214_b200 as bn
+    from paper_2106_15214_b200 import _native, parallel, solver
+
+    c = CONFIGS[args.config]
+    align = 65536 if args.config == 4 else 4
+    n0, n1 = parallel.balanced_blocks(c["N"], world, align)[rank]
+    v = make_data(args.config, n0, n1, c["dtype"])
+    w0, h0 = make_init(args.config, n0, n1)
+    config = bn.SolverConfig(beta=c["beta"], rank=c["K"], algorithm=args.algo, tol=1e-300,
+                             kappa=c["kappa"], max_outer_iters=args.warmup + args.steps)
+    kappa = parallel.resolve_kappa_global(v, c["beta"], c["kappa"]) if world > 1 else (
+        c["kappa"] if c["kappa"] is not None else bn.default_kappa(v, c["beta"]))
+
+    # ---- device-timed region: W warm-up + K timed iterations -------------
+    ctx = solver.get_context(local, c["dtype"])
+    if world > 1:
+        solver._attach_comm(ctx, c["N"])
+    ctx.set_dense(v, kappa)
+    ctx.set_factors(w0, h0)
+    ctx.begin(solver.make_params(config, kappa, kkt=False, schedule=args.schedule),
+              args.warmup + args.steps)
+    ctx.set_profiling(True)
+    ctx.step(args.warmup)
+    ctx.sync()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(local)
+    with clocks:
+        ms = ctx.step_timed(args.steps)
+    pass_ms, pass_samples = ctx.pass_time()
+    done, _ = ctx.sync()
+    obj, _, _ = ctx.trace(done)
+    launches = ctx.launches_per_iter()
+    sched = ctx.schedule()
+    ms_all = parallel.allreduce_scalars([ms, pass_ms], "max") if world > 1 else [ms, pass_ms]
+    ms, pass_ms = float(ms_all[0]), float(ms_all[1])
+    value = args.steps / (ms / 1e3)
+
+    # ---- end to end: the public API on host buffers ----------------------
+    e2e = None
+    if not args.no_e2e:
+        import torch
+        vp = torch.from_numpy(v).pin_memory().numpy()
+        cfg_e = bn.SolverConfig(beta=c["beta"], rank=c["K"], algorithm=args.algo, tol=1e-300,
+                                kappa=kappa, max_outer_iters=args.steps)
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        res = bn.fit(vp, cfg_e, init=(w0, h0), dtype=c["dtype"], kkt=False,
+                     schedule=args.schedule, sharded=world > 1)
+        _ = res.trace[-1].objective
+        te = time.perf_counter() - t0
+        te = float(parallel.allreduce_scalars([te], "max")[0]) if world > 1 else te
+        h2d = v.nbytes + w0.nbytes + h0.nbytes
+        d2h = res.factors.w.nbytes + res.factors.h.nbytes + 24 * args.steps
+        e2e = {"value": args.steps / te, "unit": "iterations/s",
+               "h2d_bytes_per_step": int(h2d * world / args.steps),
+               "d2h_bytes_per_step": int(d2h * world / args.steps),
+               "note": "one fit() call on pinned host V: upload, host-side domain checks, "
+                       f"{args.steps} iterations, download of W, H and trace"}
+
+    if rank != 0:
+        return
+    hbm, _, peak_src = measured_peaks()
+    esize = 4 if c["dtype"] == "fp32" else 8
+    vbytes_local = c["F"] * (n1 - n0) * esize
+    achieved = vbytes_local / (pass_ms / 1e3) / 1e9 if pass_ms > 0 else None
+    roofline = {
+        "bound": "hbm", "kernel": "fused_pass" if sched == "fused" else "hside_pass",
+        "achieved": achieved, "peak": hbm, "unit": "GB/s",
+        "frac": achieved / hbm if achieved else None, "traffic": None,
+        "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
+        "algorithmic_bytes_per_launch": vbytes_local,
+        "launch_ms": pass_ms, "launch_samples": pass_samples,
+        "iteration_roofline_ms": c["F"] * c["N"] * esize / world / (hbm * 1e9) * 1e3,
+        "iteration_frac": (c["F"] * c["N"] * esize / world / (hbm * 1e9) * 1e3) / (ms / args.steps),
+    }
+    out = {
+        "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32" if c["dtype"] == "fp32" else "f64", "data": "synthetic",
+        "config": workload_config(args, world), "schedule": sched,
+        "gpu_launches": launches * args.steps, "roofline": roofline,
+        "clocks": clocks.summary(), "final_objective": float(obj[-1]) if done else None,
+    }
+    if e2e:
+        out["e2e"] = e2e
+    if world == 1 and not args.no_cpu:
+        val, info = cpu_sample(args.config, args.algo)
+        out["cpu_baseline"] = {
+            "value": val, "unit": "iterations/s", "cores": info["cores"], "kind": "port",
+            "sample": f"numpy oracle (reference loop restated), fp64, {c['F']}x{info['n_sample']} "
+                      f"prefix, 3 iterations, scaled x{info['scale']:g} to N={c['N']}"}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

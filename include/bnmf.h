@@ -109,6 +109,10 @@ int bnmf_run(bnmf_ctx* ctx, const bnmf_params* p, int64_t max_iters,
 /* Introspection for the bench / tests. */
 int bnmf_launches_per_iter(bnmf_ctx* ctx, int* launches);
 int bnmf_active_schedule(bnmf_ctx* ctx, int* schedule);
+/* CUDA events around the dominant V-pass kernel of every iteration slot;
+ * bnmf_pass_time returns its average device time over the last chunk. */
+int bnmf_set_profiling(bnmf_ctx* ctx, int on);
+int bnmf_pass_time(bnmf_ctx* ctx, float* ms_avg, int* samples);
 void* bnmf_stream(bnmf_ctx* ctx);
 
 #ifdef __cplusplus

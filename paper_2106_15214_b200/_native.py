@@ -71,6 +71,8 @@ _SIGS = {
     "bnmf_launches_per_iter": ([C.c_void_p, C.POINTER(C.c_int)], C.c_int),
     "bnmf_active_schedule": ([C.c_void_p, C.POINTER(C.c_int)], C.c_int),
     "bnmf_stream": ([C.c_void_p], C.c_void_p),
+    "bnmf_set_profiling": ([C.c_void_p, C.c_int], C.c_int),
+    "bnmf_pass_time": ([C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_int)], C.c_int),
 }
 
 
@@ -225,6 +227,15 @@ class Context:
         n = C.c_int(0)
         self._check(self.lib.bnmf_launches_per_iter(self.h, C.byref(n)))
         return n.value
+
+    def set_profiling(self, on=True):
+        self._check(self.lib.bnmf_set_profiling(self.h, 1 if on else 0))
+
+    def pass_time(self):
+        ms = C.c_float(0.0)
+        n = C.c_int(0)
+        self._check(self.lib.bnmf_pass_time(self.h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     def schedule(self):
         n = C.c_int(0)

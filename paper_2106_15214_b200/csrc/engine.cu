@@ -94,11 +94,27 @@ struct Engine : EngineBase {
   int launches = 0;
   int counting = 0;
   FusedState* fused = nullptr;
+  // CUDA events around the dominant kernel of each graph slot (bench roofline)
+  static constexpr int kChunk = 16;
+  cudaEvent_t ev_a[kChunk] = {}, ev_b[kChunk] = {};
+  bool prof = false;
+  int prof_slots = 0;
 
   explicit Engine(int dev, int dt) { device = dev; dtype = dt; }
 
+  int prof_mark(bool start, int slot) {
+    if (!prof || slot >= kChunk) return 0;
+    CK(cudaEventRecord(start ? ev_a[slot] : ev_b[slot], stream));
+    if (!start) prof_slots = std::max(prof_slots, slot + 1);
+    return 0;
+  }
+
   ~Engine() override {
     if (gexec) cudaGraphExecDestroy(gexec);
+    for (int i = 0; i < kChunk; ++i) {
+      if (ev_a[i]) cudaEventDestroy(ev_a[i]);
+      if (ev_b[i]) cudaEventDestroy(ev_b[i]);
+    }
     T* tp[] = {V, Wt, Wc, Ht, Hc, C1h, C2h, C1w, C2w};
     for (T* q : tp) if (q) cudaFree(q);
     double* dp[] = {wpart, comm, opart, hpart, norms, colsum, tr_obj, tr_sec, tr_kkt};
@@ -399,7 +415,9 @@ struct Engine : EngineBase {
         if ((rc = w_update(Wt, Ht, C1h, C2h, Wt, Wc, slot))) return rc;
         if ((rc = chi(Wc, Wt, C1w, C2w, fk, slot))) return rc;
         if (den_ones && (rc = colsums(C2w, slot))) return rc;
+        if (l == 0 && (rc = prof_mark(true, slot))) return rc;
         if ((rc = hside(PM_UPDATE, Wt, Ht, C1w, C2w, Ht, Hc, den_ones, slot))) return rc;
+        if (l == 0 && (rc = prof_mark(false, slot))) return rc;
       }
     } else {
       for (int l = 0; l < Lw; ++l) {
@@ -409,7 +427,9 @@ struct Engine : EngineBase {
       for (int l = 0; l < Lh; ++l) {
         const T* hcur = l == 0 ? Ht : Hc;
         if (den_ones && (rc = colsums(Wc, slot))) return rc;
+        if (l == 0 && (rc = prof_mark(true, slot))) return rc;
         if ((rc = hside(PM_UPDATE, Wc, hcur, Wc, Wc, hcur, Hc, den_ones, slot))) return rc;
+        if (l == 0 && (rc = prof_mark(false, slot))) return rc;
       }
     }
     // objective of the unnormalised new iterate (solver.py:304-309)
@@ -469,7 +489,14 @@ struct Engine : EngineBase {
 
   int enqueue_iteration(int slot) {
     if (fused_active) {
-      if (fused_enqueue_iteration(fused, io(), slot, err)) return fail(BNMF_E_CUDA, err);
+      FusedIO o = io();
+      if (prof && slot < kChunk) { o.ev_a = ev_a[slot]; o.ev_b = ev_b[slot]; prof_slots = std::max(prof_slots, slot + 1); }
+      if (fused_enqueue_iteration(fused, o, slot, err)) return fail(BNMF_E_CUDA, err);
+      if (p.compute_kkt) {
+        // the KKT passes read the normalised iterate from the standard buffers
+        if (fused_select(fused, o, err)) return fail(BNMF_E_CUDA, err);
+        return enqueue_kkt(slot);
+      }
       return 0;
     }
     return enqueue_reference_iteration(slot);
@@ -520,6 +547,7 @@ struct Engine : EngineBase {
     if (gexec) { CK(cudaGraphExecDestroy(gexec)); gexec = nullptr; }
     fused_active = (sched == BNMF_SCHED_FUSED);
     if (fused_active) {
+      if (fused && !fused_shape_matches(fused, F, N, K)) { fused_destroy(fused); fused = nullptr; }
       if (!fused && fused_create(&fused, io(), err)) return fail(BNMF_E_CUDA, err);
       if (fused_begin(fused, io(), err)) return fail(BNMF_E_CUDA, err);
     }
@@ -555,7 +583,7 @@ struct Engine : EngineBase {
   int step(int64_t n) override {
     if (!begun) return fail(BNMF_E_STATE, "begin must precede step");
     CK(cudaSetDevice(device));
-    const int chunk = 16;
+    const int chunk = kChunk;
     int64_t full = n / chunk, rest = n % chunk;
     if (full > 0) {
       if (int rc = capture(chunk)) return rc;
@@ -587,6 +615,34 @@ struct Engine : EngineBase {
     if (sec) CK(cudaMemcpyAsync(sec, tr_sec, n * sizeof(double), cudaMemcpyDeviceToHost, stream));
     if (kkt) CK(cudaMemcpyAsync(kkt, tr_kkt, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
+    return 0;
+  }
+
+  int set_profiling(int on) override {
+    CK(cudaSetDevice(device));
+    if (on && !ev_a[0]) {
+      for (int i = 0; i < kChunk; ++i) {
+        CK(cudaEventCreate(&ev_a[i]));
+        CK(cudaEventCreate(&ev_b[i]));
+      }
+    }
+    prof = on != 0;
+    prof_slots = 0;
+    if (gexec) { CK(cudaGraphExecDestroy(gexec)); gexec = nullptr; }
+    return 0;
+  }
+
+  int pass_time(float* ms_avg, int* samples) override {
+    CK(cudaStreamSynchronize(stream));
+    double tot = 0.0;
+    int n = 0;
+    for (int i = 0; i < prof_slots; ++i) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, ev_a[i], ev_b[i]) == cudaSuccess) { tot += t; ++n; }
+    }
+    cudaGetLastError();
+    *ms_avg = n ? float(tot / n) : 0.f;
+    *samples = n;
     return 0;
   }
 
@@ -748,6 +804,17 @@ int bnmf_launches_per_iter(bnmf_ctx* ctx, int* launches) {
   CTX_CHECK(ctx);
   *launches = ctx->eng->launches_per_iter;
   return 0;
+}
+
+int bnmf_set_profiling(bnmf_ctx* ctx, int on) {
+  CTX_CHECK(ctx);
+  return ctx->eng->set_profiling(on);
+}
+
+int bnmf_pass_time(bnmf_ctx* ctx, float* ms_avg, int* samples) {
+  CTX_CHECK(ctx);
+  if (!ms_avg || !samples) return set_err("null output", BNMF_E_ARG);
+  return ctx->eng->pass_time(ms_avg, samples);
 }
 
 int bnmf_active_schedule(bnmf_ctx* ctx, int* schedule) {

@@ -35,6 +35,8 @@ struct EngineBase {
   virtual int sync(int64_t* done, int* conv) = 0;
   virtual int read_trace(double* obj, double* sec, double* kkt, int64_t n) = 0;
   virtual int init_comm(int rank, int nranks, const void* id, int64_t n_global) = 0;
+  virtual int set_profiling(int on) = 0;
+  virtual int pass_time(float* ms_avg, int* samples) = 0;
 };
 
 // What the fused fp32 pass needs from the engine (device pointers are owned by
@@ -57,6 +59,7 @@ struct FusedIO {
   ncclComm_t nccl = nullptr;
   int64_t n_global = 0;
   int* launches = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // optional, around the pass kernel
 };
 
 struct FusedState;
@@ -65,6 +68,8 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err);
 int fused_begin(FusedState* fs, const FusedIO& io, std::string& err);
 int fused_enqueue_iteration(FusedState* fs, const FusedIO& io, int slot, std::string& err);
 int fused_export(FusedState* fs, const FusedIO& io, std::string& err);
+int fused_select(FusedState* fs, const FusedIO& io, std::string& err);  // async, no sync
 void fused_destroy(FusedState* fs);
+bool fused_shape_matches(const FusedState* fs, int F, int N, int K);
 
 }  // namespace bnmf

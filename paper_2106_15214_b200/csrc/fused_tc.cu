@@ -1,21 +1,222 @@
-// Fused single-read fp32 pass (tcgen05 / TMEM / TMA) -- see DESIGN.md.
-// Placeholder until the tensor-core kernel lands: reports "unsupported" so
-// the engine uses the reference-order schedule.
+// Fused single-read schedule (fp32, sub_iters == 1): host orchestration.
+//
+// Per outer iteration p (one CUDA-graph slot):
+//   pass p            one read of V: H update of iteration p, objective of
+//                     iterate p, W-side partial sums of iteration p+1
+//   fused_reduce      fixed-order sum of the per-CTA partials -> comm
+//   ncclAllReduce     (N-sharded runs) comm across ranks
+//   finish_iter       trace row p + stop rule (solver.py:309-319)
+//   fused_update      W_{p+1}, norms, W~_{p+1}, chi maps for pass p+1
+// The pass kernel is the tcgen05 kernel (fused_pass_tc, see fused_tc_kernel.cuh)
+// when its shape limits hold, else the SIMT twin (fused_simt.cuh).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <string>
+
 #include "engine.h"
+#include "fused_simt.cuh"
+#include "small_kernels.cuh"
 
 namespace bnmf {
 
-struct FusedState { int dummy; };
+struct FusedState {
+  int F = 0, N = 0, K = 0;
+  float* H[2] = {nullptr, nullptr};
+  float* W2[2] = {nullptr, nullptr};
+  float* Wn = nullptr;
+  float* C1 = nullptr;
+  float* C2 = nullptr;
+  double* norms = nullptr;
+  double* csum2 = nullptr;
+  double* part = nullptr;
+  double* opart = nullptr;
+  int G = 0;
+  int bc = BC_GEN;
+  size_t smem = 0;
+};
 
-bool fused_supported(int, int, int, int, int, int, int, double) { return false; }
-int fused_create(FusedState** out, const FusedIO&, std::string& err) {
-  *out = nullptr; err = "fused pass not built"; return -1;
+#define FCK(call)                                                           \
+  do {                                                                      \
+    cudaError_t e_ = (call);                                                \
+    if (e_ != cudaSuccess) {                                                \
+      err = std::string(#call) + ": " + cudaGetErrorString(e_);             \
+      return -1;                                                            \
+    }                                                                       \
+  } while (0)
+
+bool fused_supported(int dtype, int F, int K, int algorithm, int L, int Lw, int Lh, double beta) {
+  (void)F; (void)beta;
+  if (dtype != BNMF_FP32) return false;
+  if (K > FS_KMAX) return false;
+  if (algorithm == BNMF_JMM) return L == 1;
+  return Lw == 1 && Lh == 1;
 }
-int fused_begin(FusedState*, const FusedIO&, std::string& err) { err = "fused pass not built"; return -1; }
-int fused_enqueue_iteration(FusedState*, const FusedIO&, int, std::string& err) {
-  err = "fused pass not built"; return -1;
+
+static size_t simt_smem(int K) {
+  int ks = kstride(K);
+  return size_t(2 * ST_NC * ks + 3 * ST_TF * ks + 2 * ST_TF * (ST_NC + 1)) * sizeof(float);
 }
-int fused_export(FusedState*, const FusedIO&, std::string&) { return 0; }
-void fused_destroy(FusedState* fs) { delete fs; }
+
+int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
+  FusedState* fs = new FusedState;
+  *out = fs;
+  fs->F = io.F; fs->N = io.N; fs->K = io.K;
+  size_t fk = size_t(io.F) * io.K, nk = size_t(io.N) * io.K;
+  FCK(cudaMalloc(&fs->H[0], nk * sizeof(float)));
+  FCK(cudaMalloc(&fs->H[1], nk * sizeof(float)));
+  FCK(cudaMalloc(&fs->W2[0], fk * sizeof(float)));
+  FCK(cudaMalloc(&fs->W2[1], fk * sizeof(float)));
+  FCK(cudaMalloc(&fs->Wn, fk * sizeof(float)));
+  FCK(cudaMalloc(&fs->C1, fk * sizeof(float)));
+  FCK(cudaMalloc(&fs->C2, fk * sizeof(float)));
+  FCK(cudaMalloc(&fs->norms, io.K * sizeof(double)));
+  FCK(cudaMalloc(&fs->csum2, io.K * sizeof(double)));
+  int nblocks = (io.N + ST_NC - 1) / ST_NC;
+  fs->G = std::max(1, std::min(nblocks, 2 * 148));
+  FCK(cudaMalloc(&fs->part, size_t(fs->G) * 2 * fk * sizeof(double)));
+  FCK(cudaMalloc(&fs->opart, size_t(fs->G) * sizeof(double)));
+  fs->smem = simt_smem(io.K);
+  return 0;
+}
+
+void fused_destroy(FusedState* fs) {
+  if (!fs) return;
+  float* fp[] = {fs->H[0], fs->H[1], fs->W2[0], fs->W2[1], fs->Wn, fs->C1, fs->C2};
+  for (float* q : fp) if (q) cudaFree(q);
+  double* dp[] = {fs->norms, fs->csum2, fs->part, fs->opart};
+  for (double* q : dp) if (q) cudaFree(q);
+  delete fs;
+}
+
+static FusedArgs make_args(FusedState* fs, const FusedIO& io, int do_h) {
+  FusedArgs a;
+  a.V = io.V; a.ldv = (long long)io.ldv;
+  a.F = io.F; a.N = io.N; a.K = io.K;
+  a.Hbuf[0] = fs->H[0]; a.Hbuf[1] = fs->H[1];
+  a.Hout[0] = fs->H[0]; a.Hout[1] = fs->H[1];
+  a.Wt2[0] = fs->W2[0]; a.Wt2[1] = fs->W2[1];
+  a.Wn = fs->Wn; a.C1 = fs->C1; a.C2 = fs->C2;
+  a.norms = fs->norms; a.csum2 = fs->csum2;
+  a.part = fs->part; a.opart = fs->opart;
+  a.algorithm = io.algorithm;
+  a.do_h = do_h;
+  a.den_ones = beta_class(io.sc.beta) == BC_1 ? 1 : 0;
+  a.sc = io.sc;
+  return a;
+}
+
+template <int BC>
+static cudaError_t launch_simt(FusedState* fs, const FusedArgs& a, const FusedIO& io, int slot,
+                               int p_override) {
+  auto kern = fused_pass_simt<BC>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fs->smem));
+  kern<<<fs->G, ST_THREADS, fs->smem, io.stream>>>(a, io.st, slot, p_override);
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_pass(FusedState* fs, const FusedArgs& a, const FusedIO& io, int slot,
+                               int p_override) {
+  switch (fs->bc) {
+    case BC_0: return launch_simt<BC_0>(fs, a, io, slot, p_override);
+    case BC_1: return launch_simt<BC_1>(fs, a, io, slot, p_override);
+    case BC_2: return launch_simt<BC_2>(fs, a, io, slot, p_override);
+    default: return launch_simt<BC_GEN>(fs, a, io, slot, p_override);
+  }
+}
+
+// pass -> reduce -> allreduce -> (finish) -> update
+static int enqueue_pass_and_update(FusedState* fs, const FusedIO& io, int slot, int p_override,
+                                   bool finish, std::string& err) {
+  FusedArgs a = make_args(fs, io, p_override == 0 ? 0 : 1);
+  size_t fk2 = size_t(2) * io.F * io.K;
+  if (io.ev_a) FCK(cudaEventRecord(io.ev_a, io.stream));
+  FCK(launch_pass(fs, a, io, slot, p_override));
+  if (io.ev_b) FCK(cudaEventRecord(io.ev_b, io.stream));
+  fused_reduce<<<int((fk2 + 1 + 255) / 256), 256, 0, io.stream>>>(
+      fs->part, fs->opart, fs->G, int(fk2), io.comm, io.st, slot, p_override);
+  FCK(cudaGetLastError());
+  if (io.launches) *io.launches += 2;
+  if (io.nranks > 1) {
+    ncclResult_t r = ncclAllReduce(io.comm, io.comm, fk2 + 1, ncclDouble, ncclSum, io.nccl,
+                                   io.stream);
+    if (r != ncclSuccess) { err = std::string("ncclAllReduce: ") + ncclGetErrorString(r); return -1; }
+    if (io.launches) *io.launches += 1;
+  }
+  if (finish) {
+    finish_iter<<<1, 1, 0, io.stream>>>(io.st, slot, io.comm + fk2, io.tr_obj, io.tr_sec,
+                                        io.sc.tol);
+    FCK(cudaGetLastError());
+    if (io.launches) *io.launches += 1;
+  }
+  WPair wp;
+  wp.w[0] = fs->W2[0]; wp.w[1] = fs->W2[1];
+  fused_update<<<io.K, 256, 0, io.stream>>>(io.comm, io.F, io.K, wp, fs->Wn, fs->C1, fs->C2,
+                                            fs->norms, fs->csum2, io.algorithm, a.den_ones, io.sc,
+                                            io.st, slot, p_override);
+  FCK(cudaGetLastError());
+  if (io.launches) *io.launches += 1;
+  return 0;
+}
+
+bool fused_shape_matches(const FusedState* fs, int F, int N, int K) {
+  return fs && fs->F == F && fs->N == N && fs->K == K;
+}
+
+int fused_begin(FusedState* fs, const FusedIO& io, std::string& err) {
+  fs->bc = beta_class(io.sc.beta);
+  size_t fk = size_t(io.F) * io.K, nk = size_t(io.N) * io.K;
+  // iterate 0 = the raw init: W~_0 = W0 (engine Wt), H~_0 = H0 (engine Ht)
+  FCK(cudaMemcpyAsync(fs->W2[0], io.Wt, fk * sizeof(float), cudaMemcpyDeviceToDevice, io.stream));
+  FCK(cudaMemcpyAsync(fs->H[0], io.Ht, nk * sizeof(float), cudaMemcpyDeviceToDevice, io.stream));
+  // prologue: W-side sums of iteration 1 from Vt_0 = W0 H0 + kappa
+  FusedIO pio = io;
+  pio.ev_a = pio.ev_b = nullptr;
+  pio.launches = nullptr;
+  int rc = enqueue_pass_and_update(fs, pio, 0, 0, false, err);
+  if (rc) return rc;
+  FCK(cudaStreamSynchronize(io.stream));
+  return 0;
+}
+
+int fused_enqueue_iteration(FusedState* fs, const FusedIO& io, int slot, std::string& err) {
+  begin_iter<<<1, 1, 0, io.stream>>>(io.st, slot);
+  FCK(cudaGetLastError());
+  if (io.launches) *io.launches += 1;
+  return enqueue_pass_and_update(fs, io, slot, -1, true, err);
+}
+
+// Copy the iterate of parity(iters_done) into the engine's Wt / Ht.
+__global__ void select_iterate(const RunState* st, const float* W0, const float* W1,
+                               const float* H0, const float* H1, float* Wt, float* Ht,
+                               size_t fk, size_t nk) {
+  int par = int(st->iters_done & 1);
+  const float* W = par ? W1 : W0;
+  const float* H = par ? H1 : H0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < fk + nk;
+       i += (size_t)gridDim.x * blockDim.x) {
+    if (i < fk) Wt[i] = W[i];
+    else Ht[i - fk] = H[i - fk];
+  }
+}
+
+int fused_select(FusedState* fs, const FusedIO& io, std::string& err) {
+  size_t fk = size_t(io.F) * io.K, nk = size_t(io.N) * io.K;
+  int blocks = int(std::min<size_t>((fk + nk + 255) / 256, 148 * 8));
+  select_iterate<<<blocks, 256, 0, io.stream>>>(io.st, fs->W2[0], fs->W2[1], fs->H[0], fs->H[1],
+                                                io.Wt, io.Ht, fk, nk);
+  FCK(cudaGetLastError());
+  if (io.launches) *io.launches += 1;
+  return 0;
+}
+
+int fused_export(FusedState* fs, const FusedIO& io, std::string& err) {
+  FusedIO o = io;
+  o.launches = nullptr;
+  if (fused_select(fs, o, err)) return -1;
+  FCK(cudaStreamSynchronize(io.stream));
+  return 0;
+}
 
 }  // namespace bnmf

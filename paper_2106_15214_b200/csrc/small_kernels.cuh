@@ -8,7 +8,7 @@
 namespace bnmf {
 
 // out[i] = sum_{s < S} part[s * stride + i], fixed order (deterministic).
-__global__ void reduce_segments(const double* __restrict__ part, size_t stride, int S,
+static __global__ void reduce_segments(const double* __restrict__ part, size_t stride, int S,
                                 size_t count, double* __restrict__ out,
                                 const RunState* st, int slot) {
   if (st && !iter_active(st, slot)) return;
@@ -21,7 +21,7 @@ __global__ void reduce_segments(const double* __restrict__ part, size_t stride, 
 }
 
 // Single-block fixed-order sum of `count` doubles into *out (count small).
-__global__ void sum_small(const double* __restrict__ in, int count, double* __restrict__ out,
+static __global__ void sum_small(const double* __restrict__ in, int count, double* __restrict__ out,
                           const RunState* st, int slot) {
   if (st && !iter_active(st, slot)) return;
   __shared__ double red[32];
@@ -112,14 +112,14 @@ __global__ void scale_h(const T* __restrict__ H, size_t N, int K, const double* 
 }
 
 // Mark the start of an iteration (timer, solver.py:302).
-__global__ void begin_iter(RunState* st, int slot) {
+static __global__ void begin_iter(RunState* st, int slot) {
   if (!iter_active(st, slot)) return;
   st->t_begin = globaltimer();
 }
 
 // Objective bookkeeping + stop rule (solver.py:309-319, 174-180).
 // obj: reduced objective (global, after any allreduce).
-__global__ void finish_iter(RunState* st, int slot, const double* __restrict__ obj,
+static __global__ void finish_iter(RunState* st, int slot, const double* __restrict__ obj,
                             double* __restrict__ trace_obj, double* __restrict__ trace_sec,
                             double tol) {
   if (!iter_active(st, slot)) return;
@@ -163,7 +163,7 @@ __global__ void kkt_w_residual(const T* __restrict__ W, const double* __restrict
   }
 }
 
-__global__ void advance_base(RunState* st, int n) { st->base += n; }
+static __global__ void advance_base(RunState* st, int n) { st->base += n; }
 
 // --- layout conversion helpers (upload / download) -------------------------
 

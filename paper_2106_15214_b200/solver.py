@@ -258,18 +258,54 @@ def _unchecked_pair(w, h):
     return pair
 
 
+def _attach_comm(ctx, n_global):
+    """Join the NCCL communicator of the current process group (once per ctx)."""
+    from . import parallel
+    rank, world = parallel.dist_info()
+    key = (rank, world, n_global)
+    if getattr(ctx, "comm_key", None) == key:
+        return
+    uid = parallel.broadcast_uid(_native.Context.nccl_unique_id)
+    ctx.init_comm(rank, world, uid, n_global)
+    ctx.comm_key = key
+
+
 def _run(data, config, counter, algorithm, *, dtype="fp64", init=None, device=None,
-         kkt=True, schedule="auto"):
+         kkt=True, schedule="auto", sharded=False):
     if config.algorithm != algorithm:
         raise ValueError(f"config.algorithm must be '{algorithm.value}' for "
                          f"run_{algorithm.value}")
     if dtype not in ("fp64", "fp32"):
         raise ValueError("dtype must be 'fp64' or 'fp32'")
-    data = _prepare(data, config)
-    F, N = data.shape
-    pair = _resolve_init(init, F, N, config.rank, config.seed)
+    n0 = 0
+    if sharded:
+        # `data` is this rank's column block; kappa and the init are global
+        from . import parallel
+        if parallel.dist_info() is None:
+            raise ValueError("sharded=True needs an initialised torch.distributed group")
+        vals = data.values if isinstance(data, DataMatrix) else np.asarray(data)
+        n0, n_global = parallel.column_offsets(vals.shape[1])
+        kappa = parallel.resolve_kappa_global(vals, config.beta, config.kappa if config.kappa
+                                              is not None else (data.kappa if isinstance(
+                                                  data, DataMatrix) else None))
+        import dataclasses
+        data = _prepare(DataMatrix(vals, kappa), dataclasses.replace(config, kappa=kappa))
+        F, N = data.shape
+        if init is None:
+            pair = init_factors(F, n_global, config.rank, config.seed)
+            init = (pair.w, pair.h)
+        w0, h0 = init if not isinstance(init, FactorPair) else (init.w, init.h)
+        w0, h0 = parallel.slice_init(w0, h0, n0, N, n_global)
+        pair = _resolve_init((w0, h0), F, N, config.rank, config.seed)
+    else:
+        data = _prepare(data, config)
+        F, N = data.shape
+        n_global = N
+        pair = _resolve_init(init, F, N, config.rank, config.seed)
     ctx = get_context(device, dtype)
     with ctx.lock:
+        if sharded:
+            _attach_comm(ctx, n_global)
         ctx.set_dense(data.values, data.kappa)
         ctx.set_factors(pair.w, pair.h)
         params = make_params(config, data.kappa, kkt=kkt, schedule=schedule)

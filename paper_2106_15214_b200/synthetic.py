@@ -82,18 +82,28 @@ def _config4_chunk(endm, seed, c, n, dtype):
     return (endm @ mix + noise).astype(dtype)
 
 
-def config4(F=256, N=4194304, K=12, seed=4, dtype=np.float64, threads=None):
+def config4(F=256, N=4194304, K=12, seed=4, dtype=np.float64, threads=None,
+            col_range=None, out=None):
     """beta=1.5 hyperspectral stand-in: columns are Dirichlet(0.3) mixtures of K
     Uniform(0,1) endmember spectra plus |N(0, 0.005)| noise.
-    Generated in 65536-column chunks so every prefix is stable."""
+    Generated in 65536-column chunks so every prefix is stable.  ``col_range``
+    = (n0, n1) returns only those columns of the N-column matrix (n0 must be a
+    chunk boundary), which is how each rank builds its own shard."""
     endm = np.random.default_rng([seed, 0xE0D]).random((F, K))
-    out = np.empty((F, N), dtype=dtype)
-    nchunks = (N + CHUNK - 1) // CHUNK
+    n0, n1 = col_range if col_range is not None else (0, N)
+    if n0 % CHUNK:
+        raise ValueError("col_range must start on a 65536-column chunk boundary")
+    if out is None:
+        out = np.empty((F, n1 - n0), dtype=dtype)
+    nchunks = (n1 - n0 + CHUNK - 1) // CHUNK
+    c_first = n0 // CHUNK
 
-    def work(c):
+    def work(i):
+        c = c_first + i
         lo = c * CHUNK
-        hi = min(N, lo + CHUNK)
-        out[:, lo:hi] = _config4_chunk(endm, seed, c, hi - lo, dtype)
+        hi = min(n1, lo + CHUNK)
+        # always draw the whole chunk so that every prefix / shard is stable
+        out[:, lo - n0:hi - n0] = _config4_chunk(endm, seed, c, CHUNK, out.dtype)[:, :hi - lo]
 
     threads = threads or min(8, os.cpu_count() or 1)
     if nchunks == 1 or threads == 1:

@@ -104,7 +104,7 @@ struct Engine : EngineBase {
 
   int prof_mark(bool start, int slot) {
     if (!prof || slot >= kChunk) return 0;
-    CK(cudaEventRecord(start ? ev_a[slot] : ev_b[slot], stream));
+    CK(cudaEventRecordWithFlags(start ? ev_a[slot] : ev_b[slot], stream, cudaEventRecordExternal));
     if (!start) prof_slots = std::max(prof_slots, slot + 1);
     return 0;
   }

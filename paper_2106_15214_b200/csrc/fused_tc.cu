@@ -13,10 +13,14 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
+
+#include <cuda.h>
 
 #include "engine.h"
 #include "fused_simt.cuh"
+#include "fused_tc_kernel.cuh"
 #include "small_kernels.cuh"
 
 namespace bnmf {
@@ -35,7 +39,42 @@ struct FusedState {
   int G = 0;
   int bc = BC_GEN;
   size_t smem = 0;
+  // tensor-core pass
+  bool tc = false;
+  int tc_grid = 0;
+  int tc_nstage = 0;
+  size_t tc_smem = 0;
+  CUtensorMap mapH, mapW;
 };
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+bool fused_tc_shape_ok(int F, int K) {
+  return F >= 1 && F <= 256 && K >= 1 && K <= ftc::KP;
+}
+
+static int tc_pick_stages(int F, size_t* bytes) {
+  for (int ns = 8; ns >= 2; --ns) {
+    size_t b = ftc::tc_layout(F, ns).bytes + 1024;
+    if (b <= 232448) { *bytes = b; return ns; }
+  }
+  return 0;
+}
 
 #define FCK(call)                                                           \
   do {                                                                      \
@@ -75,9 +114,38 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
   FCK(cudaMalloc(&fs->csum2, io.K * sizeof(double)));
   int nblocks = (io.N + ST_NC - 1) / ST_NC;
   fs->G = std::max(1, std::min(nblocks, 2 * 148));
-  FCK(cudaMalloc(&fs->part, size_t(fs->G) * 2 * fk * sizeof(double)));
-  FCK(cudaMalloc(&fs->opart, size_t(fs->G) * sizeof(double)));
   fs->smem = simt_smem(io.K);
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const char* force_simt = getenv("BNMF_FUSED_SIMT");
+  fs->tc = fused_tc_shape_ok(io.F, io.K) && encode_fn() != nullptr &&
+           !(force_simt && force_simt[0] == '1');
+  if (fs->tc) {
+    fs->tc_nstage = tc_pick_stages(io.F, &fs->tc_smem);
+    int nb = (io.N + ftc::BN - 1) / ftc::BN;
+    fs->tc_grid = std::max(1, std::min(nb, nsm));
+    if (fs->tc_nstage == 0) fs->tc = false;
+  }
+  int gmax = std::max(fs->G, fs->tc_grid);
+  FCK(cudaMalloc(&fs->part, size_t(gmax) * 2 * fk * sizeof(double)));
+  FCK(cudaMalloc(&fs->opart, size_t(gmax) * sizeof(double)));
+  if (fs->tc) {
+    cuuint64_t dims[2] = {cuuint64_t(io.N), cuuint64_t(io.F)};
+    cuuint64_t strides[1] = {cuuint64_t(io.ldv) * 4};
+    cuuint32_t boxh[2] = {128, 32}, boxw[2] = {32, 128}, es[2] = {1, 1};
+    EncodeTiledFn enc = encode_fn();
+    CUresult r1 = enc(&fs->mapH, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(io.V), dims,
+                      strides, boxh, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r2 = enc(&fs->mapW, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(io.V), dims,
+                      strides, boxw, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) {
+      err = "cuTensorMapEncodeTiled failed";
+      return -1;
+    }
+  }
   return 0;
 }
 
@@ -116,8 +184,27 @@ static cudaError_t launch_simt(FusedState* fs, const FusedArgs& a, const FusedIO
   return cudaGetLastError();
 }
 
+template <int FBC>
+static cudaError_t launch_tc(FusedState* fs, const FusedArgs& a, const FusedIO& io, int slot,
+                             int p_override) {
+  auto kern = ftc::fused_pass_tc<FBC>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fs->tc_smem));
+  kern<<<fs->tc_grid, ftc::NTHREADS, fs->tc_smem, io.stream>>>(a, fs->mapH, fs->mapW,
+                                                               fs->tc_nstage, io.st, slot,
+                                                               p_override);
+  return cudaGetLastError();
+}
+
 static cudaError_t launch_pass(FusedState* fs, const FusedArgs& a, const FusedIO& io, int slot,
                                int p_override) {
+  if (fs->tc) {
+    const double beta = io.sc.beta;
+    if (beta == 1.5) return launch_tc<ftc::FBC_15>(fs, a, io, slot, p_override);
+    if (beta == 0.0) return launch_tc<ftc::FBC_0>(fs, a, io, slot, p_override);
+    if (beta == 1.0) return launch_tc<ftc::FBC_1>(fs, a, io, slot, p_override);
+    if (beta == 2.0) return launch_tc<ftc::FBC_2>(fs, a, io, slot, p_override);
+    return launch_tc<ftc::FBC_GEN>(fs, a, io, slot, p_override);
+  }
   switch (fs->bc) {
     case BC_0: return launch_simt<BC_0>(fs, a, io, slot, p_override);
     case BC_1: return launch_simt<BC_1>(fs, a, io, slot, p_override);
@@ -131,11 +218,12 @@ static int enqueue_pass_and_update(FusedState* fs, const FusedIO& io, int slot, 
                                    bool finish, std::string& err) {
   FusedArgs a = make_args(fs, io, p_override == 0 ? 0 : 1);
   size_t fk2 = size_t(2) * io.F * io.K;
-  if (io.ev_a) FCK(cudaEventRecord(io.ev_a, io.stream));
+  if (io.ev_a) FCK(cudaEventRecordWithFlags(io.ev_a, io.stream, cudaEventRecordExternal));
   FCK(launch_pass(fs, a, io, slot, p_override));
-  if (io.ev_b) FCK(cudaEventRecord(io.ev_b, io.stream));
+  if (io.ev_b) FCK(cudaEventRecordWithFlags(io.ev_b, io.stream, cudaEventRecordExternal));
   fused_reduce<<<int((fk2 + 1 + 255) / 256), 256, 0, io.stream>>>(
-      fs->part, fs->opart, fs->G, int(fk2), io.comm, io.st, slot, p_override);
+      fs->part, fs->opart, fs->tc ? fs->tc_grid : fs->G, int(fk2), io.comm, io.st, slot,
+      p_override);
   FCK(cudaGetLastError());
   if (io.launches) *io.launches += 2;
   if (io.nranks > 1) {

@@ -63,7 +63,7 @@ def build(verbose=False, force=False):
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xptxas", "-v" if verbose else "-O3", f"-I{inc}", f"-I{os.path.join(ROOT, 'include')}",
               "--expt-relaxed-constexpr"]
-    if os.environ.get("BNMF_WATCHDOG", "1") == "1":
+    if os.environ.get("BNMF_WATCHDOG", "0") == "1":
         common.append("-DBNMF_WATCHDOG")
     srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
 

@@ -104,7 +104,7 @@ struct Engine : EngineBase {
 
   int prof_mark(bool start, int slot) {
     if (!prof || slot >= kChunk) return 0;
-    CK(cudaEventRecordWithFlags(start ? ev_a[slot] : ev_b[slot], stream, cudaEventRecordExternal));
+    CK(record_event(start ? ev_a[slot] : ev_b[slot], stream));
     if (!start) prof_slots = std::max(prof_slots, slot + 1);
     return 0;
   }

@@ -62,6 +62,15 @@ struct FusedIO {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // optional, around the pass kernel
 };
 
+// Record an event so that it also works inside stream capture (external
+// event node); outside capture a plain record.
+inline cudaError_t record_event(cudaEvent_t ev, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  if (cs == cudaStreamCaptureStatusActive) return cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
+  return cudaEventRecord(ev, s);
+}
+
 struct FusedState;
 bool fused_supported(int dtype, int F, int K, int algorithm, int L, int Lw, int Lh, double beta);
 int fused_create(FusedState** out, const FusedIO& io, std::string& err);

@@ -184,10 +184,10 @@ static cudaError_t launch_simt(FusedState* fs, const FusedArgs& a, const FusedIO
   return cudaGetLastError();
 }
 
-template <int FBC>
+template <int FBC, bool KAPPA>
 static cudaError_t launch_tc(FusedState* fs, const FusedArgs& a, const FusedIO& io, int slot,
                              int p_override) {
-  auto kern = ftc::fused_pass_tc<FBC>;
+  auto kern = ftc::fused_pass_tc<FBC, KAPPA>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fs->tc_smem));
   kern<<<fs->tc_grid, ftc::NTHREADS, fs->tc_smem, io.stream>>>(a, fs->mapH, fs->mapW,
                                                                fs->tc_nstage, io.st, slot,
@@ -195,15 +195,22 @@ static cudaError_t launch_tc(FusedState* fs, const FusedArgs& a, const FusedIO& 
   return cudaGetLastError();
 }
 
+template <int FBC>
+static cudaError_t launch_tc_k(FusedState* fs, const FusedArgs& a, const FusedIO& io, int slot,
+                               int p_override) {
+  if (io.sc.kappa != 0.0) return launch_tc<FBC, true>(fs, a, io, slot, p_override);
+  return launch_tc<FBC, false>(fs, a, io, slot, p_override);
+}
+
 static cudaError_t launch_pass(FusedState* fs, const FusedArgs& a, const FusedIO& io, int slot,
                                int p_override) {
   if (fs->tc) {
     const double beta = io.sc.beta;
-    if (beta == 1.5) return launch_tc<ftc::FBC_15>(fs, a, io, slot, p_override);
-    if (beta == 0.0) return launch_tc<ftc::FBC_0>(fs, a, io, slot, p_override);
-    if (beta == 1.0) return launch_tc<ftc::FBC_1>(fs, a, io, slot, p_override);
-    if (beta == 2.0) return launch_tc<ftc::FBC_2>(fs, a, io, slot, p_override);
-    return launch_tc<ftc::FBC_GEN>(fs, a, io, slot, p_override);
+    if (beta == 1.5) return launch_tc_k<ftc::FBC_15>(fs, a, io, slot, p_override);
+    if (beta == 0.0) return launch_tc_k<ftc::FBC_0>(fs, a, io, slot, p_override);
+    if (beta == 1.0) return launch_tc_k<ftc::FBC_1>(fs, a, io, slot, p_override);
+    if (beta == 2.0) return launch_tc_k<ftc::FBC_2>(fs, a, io, slot, p_override);
+    return launch_tc_k<ftc::FBC_GEN>(fs, a, io, slot, p_override);
   }
   switch (fs->bc) {
     case BC_0: return launch_simt<BC_0>(fs, a, io, slot, p_override);
@@ -218,9 +225,9 @@ static int enqueue_pass_and_update(FusedState* fs, const FusedIO& io, int slot, 
                                    bool finish, std::string& err) {
   FusedArgs a = make_args(fs, io, p_override == 0 ? 0 : 1);
   size_t fk2 = size_t(2) * io.F * io.K;
-  if (io.ev_a) FCK(cudaEventRecordWithFlags(io.ev_a, io.stream, cudaEventRecordExternal));
+  if (io.ev_a) FCK(record_event(io.ev_a, io.stream));
   FCK(launch_pass(fs, a, io, slot, p_override));
-  if (io.ev_b) FCK(cudaEventRecordWithFlags(io.ev_b, io.stream, cudaEventRecordExternal));
+  if (io.ev_b) FCK(record_event(io.ev_b, io.stream));
   fused_reduce<<<int((fk2 + 1 + 255) / 256), 256, 0, io.stream>>>(
       fs->part, fs->opart, fs->tc ? fs->tc_grid : fs->G, int(fk2), io.comm, io.st, slot,
       p_override);

@@ -1,27 +1,28 @@
-// tcgen05 implementation of the fused single-read pass (fp32 in 3xTF32,
-// F <= 256 rows, rank K <= 16).  Same contract as fused_pass_simt.
+// tcgen05 implementation of the fused single-read pass (fp32 carried as
+// 3xTF32, F <= 256 rows, rank K <= 16).  Same contract as fused_pass_simt.
 //
 // One persistent CTA per SM walks 128-column blocks of V.  Warp roles:
-//   warp 0      TMA producer: V tiles into a 16 KB smem ring, in the order
-//               the epilogue consumes them (per block: F/32 tiles [32 f x 128 n]
-//               for the H phase, then 4*FT tiles [128 f x 32 n], 128B
-//               swizzled, for the W phase -- the second read hits L2)
-//   warp 1      MMA issuer (one thread) + TMEM owner
-//   warps 2..9  epilogue: TMEM -> registers, the beta-dependent terms, the
-//               hi/lo TF32 split written back to TMEM as MMA A operands,
-//               the H update, the objective, fp64 folding of the W sums
-// Per block (n0 .. n0+127):
+//   warp 0      TMA producer: V tiles into a 16 KB smem ring, in consumption
+//               order (per block: F/32 tiles [32 f x 128 n] for the H phase,
+//               then 4*FT tiles [128 f x 32 n], 128B-swizzled, for the W
+//               phase -- that second read is served by L2)
+//   warp 1      MMA issuer (warp-uniform loop, elected lane issues) + TMEM owner
+//   warps 2..17 epilogue: TMEM -> registers, the beta-dependent terms, the
+//               hi/lo TF32 split written back to TMEM as MMA A operands, the
+//               H update, the objective, fp64 folding of the W sums
+// Per block (columns n0 .. n0+127):
 //   H phase, f sub-tile j (32 rows):
-//     D   [n x f]  = Hp (128x16) * Wa[j]^T           6 MMAs  M128 N32  (3xTF32)
-//     ZT  [n x f]  = Zn, Zd of (V, D + kappa)        epilogue -> TMEM
-//     AccH[n x k] += ZT * chi[j]                     24 MMAs M128 N16  (A in TMEM)
+//     D    [n x f] = Hp (128x16) * Wa[j]^T            6 MMAs  M128 N32 (3xTF32)
+//     ZT   [n x f] = Zn, Zd of (V, D + kappa)         epilogue -> TMEM
+//     AccH [n x k] += ZT * chi[j]                     24 MMAs M128 N16 (A in TMEM)
 //   H update: H~_p = Hp * (AccHn / max(AccHd, floor))^gamma * norms -> smem, HBM
 //   W phase, f tile t (128 rows) x n sub-tile u (32 cols):
-//     D   [f x n]  = W~_p[t] * H~_p[u]^T             6 MMAs  M128 N32
-//     Z   [f x n]  = Zn, Zd of (V, D + kappa); objective
-//     AccW[t]     += Z * H~_p[u]                     24 MMAs M128 N16  (A in TMEM)
-//   AccW is folded into fp64 registers once per block.
-// All smem operands are K-major "core-tiled" (8 rows x 16 B core matrices).
+//     D    [f x n] = W~_p[t] * H~_p[u]^T              6 MMAs  M128 N32
+//     Z    [f x n] = Zn, Zd of (V, D + kappa); objective
+//     AccW [t]    += Z * H~_p[u]                      24 MMAs M128 N16 (A in TMEM)
+//   AccW stays in TMEM for FOLD blocks, then is added into the CTA's fp64
+//   partial slab (fixed order => deterministic).
+// All smem MMA operands are K-major "core-tiled" (8 rows x 16 B core matrices).
 #pragma once
 
 #include <cuda.h>
@@ -36,8 +37,9 @@ using namespace bnmf::tc;
 
 constexpr int BN = 128;            // columns per block
 constexpr int KP = 16;             // padded rank
-constexpr int NEPI = 8;            // epilogue warps
+constexpr int NEPI = 16;           // epilogue warps (4 per TMEM lane quadrant)
 constexpr int NTHREADS = 32 * (2 + NEPI);
+constexpr int FOLD = 8;            // blocks accumulated in TMEM before the fp64 fold
 constexpr uint32_t STAGE_BYTES = 32 * 128 * 4;
 
 // TMEM columns
@@ -78,15 +80,15 @@ __host__ __device__ inline TcLayout tc_layout(int F, int nstage) {
 }
 
 // element (k, c) of a K-major [16 rows x C] tile whose K dimension is C:
-// (rows k, 8-row groups at SBO = C*32 bytes, 4-wide chunks of c at 128 B)
-__device__ __forceinline__ uint32_t coreT_off(int k, int c, int C) {
+// 8-row groups at SBO = C*32 bytes, 4-wide chunks of c at 128 B
+__host__ __device__ __forceinline__ uint32_t coreT_off(int k, int c, int C) {
   return uint32_t((k >> 3) * (C * 32) + (c >> 2) * 128 + (k & 7) * 16 + (c & 3) * 4);
 }
 
 template <int FBC>
 __device__ __forceinline__ void zpair(float x, float y, float beta, float& zn, float& zd) {
   if (FBC == FBC_15) {
-    float r = rsqrtf(y);
+    const float r = rsqrt_fast(y);
     zn = x * r;
     zd = y * r;
   } else if (FBC == FBC_2) {
@@ -94,7 +96,7 @@ __device__ __forceinline__ void zpair(float x, float y, float beta, float& zn, f
   } else if (FBC == FBC_1) {
     zn = __fdividef(x, y); zd = 1.f;
   } else if (FBC == FBC_0) {
-    float r = __frcp_rn(y);
+    const float r = __fdividef(1.f, y);
     zn = x * r * r; zd = r;
   } else {
     bases32<BC_GEN>(x, y, beta, zn, zd);
@@ -105,8 +107,8 @@ template <int FBC>
 __device__ __forceinline__ float dterm(float x, float y, float zd, float beta) {
   if (FBC == FBC_15) {
     // d_{3/2}(x|y) = (2/3) (sqrt x - sqrt y)^2 (2 sqrt x + sqrt y); zd = sqrt y
-    float sx = x > 0.f ? x * rsqrtf(x) : 0.f;
-    float dq = sx - zd;
+    const float sx = sqrt_fast(x);
+    const float dq = sx - zd;
     return 0.6666666666666666f * dq * dq * fmaf(2.f, sx, zd);
   } else if (FBC == FBC_2) {
     return divergence32<BC_2>(x, y, beta);
@@ -118,13 +120,46 @@ __device__ __forceinline__ float dterm(float x, float y, float zd, float beta) {
   return divergence32<BC_GEN>(x, y, beta);
 }
 
-__device__ __forceinline__ void split_store(char* base_hi, char* base_lo, uint32_t off, float v) {
-  float hi = to_tf32(v);
-  *reinterpret_cast<float*>(base_hi + off) = hi;
-  *reinterpret_cast<float*>(base_lo + off) = to_tf32(v - hi);
+// smem descriptor arithmetic: the start-address field is addr >> 4 in the low
+// 14 bits, so desc(addr + off) == desc(addr) + (off >> 4) for smem < 256 KB.
+__device__ __forceinline__ uint64_t dplus(uint64_t d, uint32_t off) { return d + (off >> 4); }
+
+// D (+)= A * B^T over K = 16 in 3xTF32: (hi,hi) + (hi,lo) + (lo,hi), 2 k-steps
+// each; A and B K-major core-tiled (LBO 128, SBO 512).
+__device__ __forceinline__ void issue_big(uint32_t dcol, uint64_t a_hi, uint64_t a_lo,
+                                          uint64_t b_hi, uint64_t b_lo, uint32_t idesc) {
+  mma_ss_elect(dcol, a_hi, b_hi, idesc, 0u);
+  mma_ss_elect(dcol, dplus(a_hi, 256), dplus(b_hi, 256), idesc, 1u);
+  mma_ss_elect(dcol, a_hi, b_lo, idesc, 1u);
+  mma_ss_elect(dcol, dplus(a_hi, 256), dplus(b_lo, 256), idesc, 1u);
+  mma_ss_elect(dcol, a_lo, b_hi, idesc, 1u);
+  mma_ss_elect(dcol, dplus(a_lo, 256), dplus(b_hi, 256), idesc, 1u);
 }
 
-template <int FBC>
+// D (+)= Z * B over a 32-wide K slab: Z (hi/lo) in TMEM columns, B K-major
+// [16 x K]; 3xTF32, 4 k-steps each.
+__device__ __forceinline__ void issue_side(uint32_t dcol, uint32_t z_hi, uint32_t z_lo,
+                                           uint64_t b_hi, uint64_t b_lo, uint32_t idesc,
+                                           bool fresh) {
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+    mma_ts_elect(dcol, z_hi + 8 * s, dplus(b_hi, 256 * s), idesc, (fresh && s == 0) ? 0u : 1u);
+#pragma unroll
+  for (int s = 0; s < 4; ++s) mma_ts_elect(dcol, z_hi + 8 * s, dplus(b_lo, 256 * s), idesc, 1u);
+#pragma unroll
+  for (int s = 0; s < 4; ++s) mma_ts_elect(dcol, z_lo + 8 * s, dplus(b_hi, 256 * s), idesc, 1u);
+}
+
+// store 8 Z values (hi/lo split) at TMEM columns col (hi) and col + 32 (lo)
+__device__ __forceinline__ void store_z8(uint32_t col, const float* z) {
+  float hi[8], lo[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { hi[i] = tf32_trunc(z[i]); lo[i] = z[i] - hi[i]; }
+  tmem_st8(col, hi);
+  tmem_st8(col + 32, lo);
+}
+
+template <int FBC, bool KAPPA>
 __global__ void __launch_bounds__(NTHREADS, 1)
 fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
               const __grid_constant__ CUtensorMap mapW, int nstage, const RunState* st, int slot,
@@ -136,21 +171,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
       (reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
   const int F = a.F, N = a.N, K = a.K;
   const TcLayout L = tc_layout(F, nstage);
-  char* s_stage = reinterpret_cast<char*>(smem + L.off_stage);
-  char* s_wa[2] = {reinterpret_cast<char*>(smem + L.off_wa),
-                   reinterpret_cast<char*>(smem + L.off_wa + L.FP * KP * 4)};
-  char* s_wt[2] = {reinterpret_cast<char*>(smem + L.off_wt),
-                   reinterpret_cast<char*>(smem + L.off_wt + L.FP * KP * 4)};
-  char* s_c1[2] = {reinterpret_cast<char*>(smem + L.off_c1),
-                   reinterpret_cast<char*>(smem + L.off_c1 + L.FP * KP * 4)};
-  char* s_c2[2] = {reinterpret_cast<char*>(smem + L.off_c2),
-                   reinterpret_cast<char*>(smem + L.off_c2 + L.FP * KP * 4)};
-  char* s_hp[2] = {reinterpret_cast<char*>(smem + L.off_hp),
-                   reinterpret_cast<char*>(smem + L.off_hp + BN * KP * 4)};
-  char* s_hn[2] = {reinterpret_cast<char*>(smem + L.off_hn),
-                   reinterpret_cast<char*>(smem + L.off_hn + BN * KP * 4)};
-  char* s_hnt[2] = {reinterpret_cast<char*>(smem + L.off_hnt),
-                    reinterpret_cast<char*>(smem + L.off_hnt + BN * KP * 4)};
+  const uint32_t s_base = smem_u32(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.off_bar);
   uint64_t* bar_full = bars;                 // [nstage]
   uint64_t* bar_empty = bars + 8;            // [nstage]
@@ -174,6 +195,8 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
   const int den_ones = a.den_ones;
   const float kappa = float(a.sc.kappa), beta = float(a.sc.beta);
   const int nblocks = (N + BN - 1) / BN;
+  const uint32_t wb = uint32_t(L.FP) * KP * 4;   // hi -> lo offset of F x 16 operands
+  const uint32_t hb = BN * KP * 4;               // hi -> lo offset of 128 x 16 operands
 
   // ---- setup: barriers, TMEM, constant operands ---------------------------
   if (threadIdx.x == 0) {
@@ -203,12 +226,16 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
       const int f = i / KP, k = i - f * KP;
       const bool ok = f < F && k < K;
       const size_t gi = size_t(f) * K + k;
-      const uint32_t o = core_off(f, k);
-      split_store(s_wa[0], s_wa[1], o, ok ? Wa[gi] : 0.f);
-      split_store(s_wt[0], s_wt[1], o, ok ? Wt[gi] : 0.f);
-      const uint32_t ot = coreT_off(k, f, L.FP);
-      split_store(s_c1[0], s_c1[1], ot, ok ? a.C1[gi] : 0.f);
-      split_store(s_c2[0], s_c2[1], ot, ok ? a.C2[gi] : 0.f);
+      const uint32_t o = core_off(f, k), ot = coreT_off(k, f, L.FP);
+      float v, hi;
+      v = ok ? Wa[gi] : 0.f; hi = tf32_hi(v);
+      sts_f32(s_base + L.off_wa + o, hi); sts_f32(s_base + L.off_wa + wb + o, v - hi);
+      v = ok ? Wt[gi] : 0.f; hi = tf32_hi(v);
+      sts_f32(s_base + L.off_wt + o, hi); sts_f32(s_base + L.off_wt + wb + o, v - hi);
+      v = ok ? a.C1[gi] : 0.f; hi = tf32_hi(v);
+      sts_f32(s_base + L.off_c1 + ot, hi); sts_f32(s_base + L.off_c1 + wb + ot, v - hi);
+      v = ok ? a.C2[gi] : 0.f; hi = tf32_hi(v);
+      sts_f32(s_base + L.off_c2 + ot, hi); sts_f32(s_base + L.off_c2 + wb + ot, v - hi);
     }
   }
   fence_async_smem();
@@ -228,177 +255,174 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
           for (int j = 0; j < L.SH; ++j) {
             mbar_wait(&bar_empty[stage], ph ^ 1);
             mbar_expect_tx(&bar_full[stage], STAGE_BYTES);
-            tma_load_2d(s_stage + stage * STAGE_BYTES, &mapH, &bar_full[stage], n0, 32 * j);
+            tma_load_2d(smem + L.off_stage + stage * STAGE_BYTES, &mapH, &bar_full[stage], n0,
+                        32 * j);
             if (++stage == nstage) { stage = 0; ph ^= 1; }
           }
         }
         for (int w = 0; w < L.SW; ++w) {
           mbar_wait(&bar_empty[stage], ph ^ 1);
           mbar_expect_tx(&bar_full[stage], STAGE_BYTES);
-          tma_load_2d(s_stage + stage * STAGE_BYTES, &mapW, &bar_full[stage], n0 + 32 * (w & 3),
-                      128 * (w >> 2));
+          tma_load_2d(smem + L.off_stage + stage * STAGE_BYTES, &mapW, &bar_full[stage],
+                      n0 + 32 * (w & 3), 128 * (w >> 2));
           if (++stage == nstage) { stage = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ======================= MMA issuer =====================================
-    if (lane == 0) {
-      const uint32_t id_big = idesc_tf32(128, 32, 0, 0);
-      const uint32_t id_side = idesc_tf32(128, 16, 0, 0);
-      const uint32_t sb_wa[2] = {smem_u32(s_wa[0]), smem_u32(s_wa[1])};
-      const uint32_t sb_wt[2] = {smem_u32(s_wt[0]), smem_u32(s_wt[1])};
-      const uint32_t sb_c1[2] = {smem_u32(s_c1[0]), smem_u32(s_c1[1])};
-      const uint32_t sb_c2[2] = {smem_u32(s_c2[0]), smem_u32(s_c2[1])};
-      const uint32_t sb_hp[2] = {smem_u32(s_hp[0]), smem_u32(s_hp[1])};
-      const uint32_t sb_hn[2] = {smem_u32(s_hn[0]), smem_u32(s_hn[1])};
-      const uint32_t sb_hnt[2] = {smem_u32(s_hnt[0]), smem_u32(s_hnt[1])};
-      const uint32_t sbo_c = uint32_t(L.FP) * 32;   // chi^T rows k, K-dim FP
-      const uint32_t sbo_hnt = BN * 32;            // H~^T rows k, K-dim 128
-      // 3xTF32 product list: (a_hi,b_hi), (a_hi,b_lo), (a_lo,b_hi)
-      const int pa[3] = {0, 0, 1}, pb[3] = {0, 1, 0};
-      uint32_t c = 0;   // sub-tile counter (D / Z double buffer)
-      int bi = 0;
-      int last_w = -1;  // pending W-side sub-tile of the previous block
-      auto issue_sideW = [&](uint32_t cc, int w, int first_of_block) {
-        const uint32_t buf = cc & 1;
+    // ======================= MMA issuer (warp-uniform) ======================
+    const uint32_t id_big = idesc_tf32(128, 32, 0, 0);
+    const uint32_t id_side = idesc_tf32(128, 16, 0, 0);
+    const uint64_t d_wa = sdesc(s_base + L.off_wa, 128, 512);
+    const uint64_t d_wt = sdesc(s_base + L.off_wt, 128, 512);
+    const uint64_t d_hp = sdesc(s_base + L.off_hp, 128, 512);
+    const uint64_t d_hn = sdesc(s_base + L.off_hn, 128, 512);
+    const uint64_t d_c1 = sdesc(s_base + L.off_c1, 128, uint32_t(L.FP) * 32);
+    const uint64_t d_c2 = sdesc(s_base + L.off_c2, 128, uint32_t(L.FP) * 32);
+    const uint64_t d_hnt = sdesc(s_base + L.off_hnt, 128, BN * 32);
+    uint32_t c = 0;       // sub-tile counter (D / Z double buffer)
+    int bi = 0;
+    int pending = -1;     // W sub-tile of the previous block still to issue
+    bool pend_fold = false;
+    // W side of sub-tile (cc, w): AccW[t] += Z * H~_p[u] (num and den)
+    auto side_w = [&](uint32_t cc, int w, bool fresh) {
+      const uint32_t zb = tmem + TM_Z + 128 * (cc & 1);
+      const int t = w >> 2, u = w & 3;
+      const uint64_t bh = dplus(d_hnt, u * 1024);
+      const uint64_t bl = dplus(bh, hb);
+      issue_side(tmem + TM_ACCW + 32 * t, zb, zb + 32, bh, bl, id_side, fresh && u == 0);
+      issue_side(tmem + TM_ACCW + 32 * t + 16, zb + 64, zb + 96, bh, bl, id_side, fresh && u == 0);
+    };
+    // H side of sub-tile (cc, j): AccH += ZT * chi[j]
+    auto side_h = [&](uint32_t cc, int j) {
+      const uint32_t zb = tmem + TM_Z + 128 * (cc & 1);
+      const uint64_t b1 = dplus(d_c1, j * 1024);
+      issue_side(tmem + TM_ACCH, zb, zb + 32, b1, dplus(b1, wb), id_side, j == 0);
+      if (!den_ones) {
+        const uint64_t b2 = dplus(d_c2, j * 1024);
+        issue_side(tmem + TM_ACCH + 16, zb + 64, zb + 96, b2, dplus(b2, wb), id_side, j == 0);
+      }
+    };
+    auto wait_z = [&](uint32_t cc) {
+      mbar_wait(&bar_zfull[cc & 1], (cc >> 1) & 1);
+      tc_fence_after();
+    };
+    auto flush_pending = [&]() {
+      if (pending >= 0) {
+        wait_z(c - 1);
+        side_w(c - 1, pending, false);
+        if (pend_fold) mma_commit_elect(bar_accw);
+        pending = -1;
+      }
+    };
+    for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++bi) {
+      const bool fresh = (bi % FOLD) == 0;
+      if (do_h) {
+        mbar_wait(bar_hp, bi & 1);
+        tc_fence_after();
+        for (int j = 0; j < L.SH; ++j, ++c) {
+          issue_big(tmem + TM_D + 32 * (c & 1), d_hp, dplus(d_hp, hb), dplus(d_wa, j * 2048),
+                    dplus(d_wa, j * 2048 + wb), id_big);
+          mma_commit_elect(&bar_dfull[c & 1]);
+          if (j > 0) {
+            wait_z(c - 1);
+            side_h(c - 1, j - 1);
+          } else {
+            flush_pending();
+          }
+        }
+        wait_z(c - 1);
+        side_h(c - 1, L.SH - 1);
+        mma_commit_elect(bar_acch);
+      } else {
+        flush_pending();
+      }
+      mbar_wait(bar_hn, bi & 1);
+      tc_fence_after();
+      for (int w = 0; w < L.SW; ++w, ++c) {
         const int t = w >> 2, u = w & 3;
-        const uint32_t zbase = tmem + TM_Z + 128 * buf;
-        for (int q = 0; q < 2; ++q) {          // num, den
-          if (q == 1 && den_ones == 2) break;  // (never: W den needs Zd = 1 for beta = 1)
-          const uint32_t dcol = tmem + TM_ACCW + 32 * t + 16 * q;
-          for (int pr = 0; pr < 3; ++pr) {
-            const uint32_t acol = zbase + 64 * q + 32 * pa[pr];
-            for (int s = 0; s < 4; ++s) {
-              const uint64_t bd = sdesc(sb_hnt[pb[pr]] + u * 1024 + s * 256, 128, sbo_hnt);
-              const uint32_t acc = (first_of_block && (u == 0) && pr == 0 && s == 0) ? 0u : 1u;
-              mma_ts(dcol, acol + 8 * s, bd, id_side, acc);
-            }
-          }
-        }
-      };
-      auto issue_sideH = [&](uint32_t cc, int j) {
-        const uint32_t buf = cc & 1;
-        const uint32_t zbase = tmem + TM_Z + 128 * buf;
-        for (int q = 0; q < 2; ++q) {
-          if (q == 1 && den_ones) break;
-          const uint32_t dcol = tmem + TM_ACCH + 16 * q;
-          const uint32_t* cb = q == 0 ? sb_c1 : sb_c2;
-          for (int pr = 0; pr < 3; ++pr) {
-            const uint32_t acol = zbase + 64 * q + 32 * pa[pr];
-            for (int s = 0; s < 4; ++s) {
-              const uint64_t bd = sdesc(cb[pb[pr]] + j * 1024 + s * 256, 128, sbo_c);
-              const uint32_t acc = (j == 0 && pr == 0 && s == 0) ? 0u : 1u;
-              mma_ts(dcol, acol + 8 * s, bd, id_side, acc);
-            }
-          }
-        }
-      };
-      for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++bi) {
-        if (do_h) {
-          mbar_wait(bar_hp, bi & 1);
-          tc_fence_after();
-          for (int j = 0; j < L.SH; ++j, ++c) {
-            const uint32_t buf = c & 1;
-            const uint32_t dcol = tmem + TM_D + 32 * buf;
-            int m = 0;
-            for (int pr = 0; pr < 3; ++pr)
-              for (int s = 0; s < 2; ++s, ++m)
-                mma_ss(dcol, sdesc(sb_hp[pa[pr]] + s * 256, 128, 512),
-                       sdesc(sb_wa[pb[pr]] + j * 2048 + s * 256, 128, 512), id_big, m > 0);
-            mma_commit(&bar_dfull[buf]);
-            if (j > 0) {
-              mbar_wait(&bar_zfull[(c - 1) & 1], ((c - 1) >> 1) & 1);
-              tc_fence_after();
-              issue_sideH(c - 1, j - 1);
-            } else if (last_w >= 0) {
-              mbar_wait(&bar_zfull[(c - 1) & 1], ((c - 1) >> 1) & 1);
-              tc_fence_after();
-              issue_sideW(c - 1, last_w, last_w < 4 ? 0 : 0);
-              mma_commit(bar_accw);
-              last_w = -1;
-            }
-          }
-          mbar_wait(&bar_zfull[(c - 1) & 1], ((c - 1) >> 1) & 1);
-          tc_fence_after();
-          issue_sideH(c - 1, L.SH - 1);
-          mma_commit(bar_acch);
-        } else if (last_w >= 0) {
-          mbar_wait(&bar_zfull[(c - 1) & 1], ((c - 1) >> 1) & 1);
-          tc_fence_after();
-          issue_sideW(c - 1, last_w, 0);
-          mma_commit(bar_accw);
-          last_w = -1;
-        }
-        mbar_wait(bar_hn, bi & 1);
-        tc_fence_after();
-        for (int w = 0; w < L.SW; ++w, ++c) {
-          const uint32_t buf = c & 1;
-          const uint32_t dcol = tmem + TM_D + 32 * buf;
-          const int t = w >> 2, u = w & 3;
-          int m = 0;
-          for (int pr = 0; pr < 3; ++pr)
-            for (int s = 0; s < 2; ++s, ++m)
-              mma_ss(dcol, sdesc(sb_wt[pa[pr]] + t * 8192 + s * 256, 128, 512),
-                     sdesc(sb_hn[pb[pr]] + u * 2048 + s * 256, 128, 512), id_big, m > 0);
-          mma_commit(&bar_dfull[buf]);
-          if (w > 0) {
-            mbar_wait(&bar_zfull[(c - 1) & 1], ((c - 1) >> 1) & 1);
+        issue_big(tmem + TM_D + 32 * (c & 1), dplus(d_wt, t * 8192), dplus(d_wt, t * 8192 + wb),
+                  dplus(d_hn, u * 2048), dplus(d_hn, u * 2048 + hb), id_big);
+        mma_commit_elect(&bar_dfull[c & 1]);
+        if (w > 0) {
+          wait_z(c - 1);
+          if (w == 1 && fresh && bi > 0) {
+            mbar_wait(bar_accw_free, ((bi / FOLD) - 1) & 1);
             tc_fence_after();
-            if (w == 1 && bi > 0) {
-              mbar_wait(bar_accw_free, (bi - 1) & 1);
-              tc_fence_after();
-            }
-            issue_sideW(c - 1, w - 1, 1);
           }
+          side_w(c - 1, w - 1, fresh);
         }
-        last_w = L.SW - 1;
       }
-      if (last_w >= 0) {
-        mbar_wait(&bar_zfull[(c - 1) & 1], ((c - 1) >> 1) & 1);
-        tc_fence_after();
-        issue_sideW(c - 1, last_w, 0);
-        mma_commit(bar_accw);
-      }
+      pending = L.SW - 1;
+      pend_fold = (bi % FOLD) == FOLD - 1 || b + (int)gridDim.x >= nblocks;
     }
+    flush_pending();
     __syncwarp();
   } else {
     // ======================= epilogue =======================================
     const int e = warp - 2;
     const int q = warp & 3;          // TMEM lane quadrant
-    const int h = e >> 2;            // column half / tile index
+    const int g = e >> 2;            // 8-column slice of a 32-wide sub-tile
     const int row = 32 * q + lane;   // TMEM lane (n in the H phase, f_local in the W phase)
     const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16);
     double obj = 0.0;
-    double accw_n[KP], accw_d[KP];
-#pragma unroll
-    for (int k = 0; k < KP; ++k) { accw_n[k] = 0.0; accw_d[k] = 0.0; }
-    float hprev[8];
+    float hprev[4];
     int stage = 0;
     uint32_t ph = 0;
     uint32_t c = 0;
     int bi = 0;
+    int nfold = 0;
+    double* mypart = a.part + size_t(blockIdx.x) * 2 * F * K;
 
-    // rows of the block's H~_{p-1} (this thread: n = row, k in [8h, 8h+8))
+    // H~_{p-1} rows of a block (this thread: n = row, k in [4g, 4g+4))
     auto load_hprev = [&](int n0) {
       const int n = n0 + row;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int k = 8 * h + i;
+      for (int i = 0; i < 4; ++i) {
+        const int k = 4 * g + i;
         hprev[i] = (n < N && k < K) ? Hprev[size_t(n) * K + k] : 0.f;
-        split_store(s_hp[0], s_hp[1], core_off(row, k), hprev[i]);
+        const float hi = tf32_hi(hprev[i]);
+        const uint32_t o = s_base + L.off_hp + core_off(row, k);
+        sts_f32(o, hi);
+        sts_f32(o + hb, hprev[i] - hi);
       }
     };
     auto store_hnew = [&](int n0, const float* hv) {
       const int n = n0 + row;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int k = 8 * h + i;
+      for (int i = 0; i < 4; ++i) {
+        const int k = 4 * g + i;
         const float v = (n < N && k < K) ? hv[i] : 0.f;
         if (do_h && n < N && k < K) Hnew[size_t(n) * K + k] = v;
-        split_store(s_hn[0], s_hn[1], core_off(row, k), v);
-        split_store(s_hnt[0], s_hnt[1], coreT_off(k, row, BN), v);
+        const float hi = tf32_hi(v);
+        const uint32_t o = s_base + L.off_hn + core_off(row, k);
+        const uint32_t ot = s_base + L.off_hnt + coreT_off(k, row, BN);
+        sts_f32(o, hi);
+        sts_f32(o + hb, v - hi);
+        sts_f32(ot, hi);
+        sts_f32(ot + hb, v - hi);
       }
+    };
+    // add the TMEM W sums of the last FOLD blocks into the fp64 slab
+    auto fold = [&]() {
+      mbar_wait(bar_accw, nfold & 1);
+      tc_fence_after();
+      if (g < 2 * L.FT) {
+        const int t = g >> 1, s = g & 1;   // tile, num/den
+        float v[16];
+        tmem_ld16(lane_base + TM_ACCW + 32 * t + 16 * s, v);
+        const int f = 128 * t + row;
+        if (f < F) {
+          double* dst = mypart + size_t(s) * F * K + size_t(f) * K;
+#pragma unroll
+          for (int k = 0; k < KP; ++k)
+            if (k < K) dst[k] = (nfold == 0 ? 0.0 : dst[k]) + double(v[k]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_accw_free);
+      ++nfold;
     };
 
     int b = blockIdx.x;
@@ -410,6 +434,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
     }
     for (; b < nblocks; b += gridDim.x, ++bi) {
       const int n0 = b * BN;
+      const bool ncols_full = n0 + BN <= N;
       if (do_h) {
         // ---------------- H phase ----------------
         for (int j = 0; j < L.SH; ++j, ++c) {
@@ -417,32 +442,26 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
           mbar_wait(&bar_dfull[buf], (c >> 1) & 1);
           mbar_wait(&bar_full[stage], ph);
           tc_fence_after();
-          float y[16], zn[16], zd[16];
-          tmem_ld16(lane_base + TM_D + 32 * buf + 16 * h, y);
-          const float* tile = reinterpret_cast<const float*>(s_stage + stage * STAGE_BYTES);
-          const bool nvalid = n0 + row < N;
+          float y[8], x[8], zn[8], zd[8];
+          tmem_ld8(lane_base + TM_D + 32 * buf + 8 * g, y);
+          const uint32_t xa = s_base + L.off_stage + stage * STAGE_BYTES + (8 * g * 128 + row) * 4;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int fl = 16 * h + i;
-            const float x = tile[fl * 128 + row];
-            const bool ok = nvalid && (32 * j + fl < F);
-            float a1 = 0.f, a2 = 0.f;
-            if (ok) zpair<FBC>(x, y[i] + kappa, beta, a1, a2);
-            zn[i] = a1;
-            zd[i] = a2;
+          for (int i = 0; i < 8; ++i) x[i] = lds_f32(xa + i * 512);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            zpair<FBC>(x[i], KAPPA ? y[i] + kappa : y[i], beta, zn[i], zd[i]);
+          if (!(ncols_full && 32 * j + 32 <= F)) {
+            const bool nok = n0 + row < N;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const bool ok = nok && (32 * j + 8 * g + i < F);
+              zn[i] = ok ? zn[i] : 0.f;
+              zd[i] = ok ? zd[i] : 0.f;
+            }
           }
-          float hi[16], lo[16];
-          const uint32_t zb = lane_base + TM_Z + 128 * buf + 16 * h;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) { hi[i] = to_tf32(zn[i]); lo[i] = to_tf32(zn[i] - hi[i]); }
-          tmem_st16(zb + 0, hi);
-          tmem_st16(zb + 32, lo);
-          if (!den_ones) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) { hi[i] = to_tf32(zd[i]); lo[i] = to_tf32(zd[i] - hi[i]); }
-            tmem_st16(zb + 64, hi);
-            tmem_st16(zb + 96, lo);
-          }
+          const uint32_t zb = lane_base + TM_Z + 128 * buf + 8 * g;
+          store_z8(zb, zn);
+          if (!den_ones) store_z8(zb + 64, zd);
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
@@ -455,12 +474,12 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
         // ---------------- H update ----------------
         mbar_wait(bar_acch, bi & 1);
         tc_fence_after();
-        float nv[8], dv[8], hv[8];
-        tmem_ld8(lane_base + TM_ACCH + 8 * h, nv);
-        if (!den_ones) tmem_ld8(lane_base + TM_ACCH + 16 + 8 * h, dv);
+        float nv[4], dv[4], hv[4];
+        tmem_ld4(lane_base + TM_ACCH + 4 * g, nv);
+        if (!den_ones) tmem_ld4(lane_base + TM_ACCH + 16 + 4 * g, dv);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int k = 8 * h + i;
+        for (int i = 0; i < 4; ++i) {
+          const int k = 4 * g + i;
           float v = 0.f;
           if (k < K) {
             const double den = den_ones ? a.csum2[k] : double(dv[i]);
@@ -491,43 +510,34 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
         mbar_wait(&bar_dfull[buf], (c >> 1) & 1);
         mbar_wait(&bar_full[stage], ph);
         tc_fence_after();
-        float y[16], zn[16], zd[16];
-        tmem_ld16(lane_base + TM_D + 32 * buf + 16 * h, y);
-        const char* tile = s_stage + stage * STAGE_BYTES;
-        const int f = 128 * t + row;
-        float x[16];
+        float y[8], x[8], zn[8], zd[8], dd[8];
+        tmem_ld8(lane_base + TM_D + 32 * buf + 8 * g, y);
+        const uint32_t ta = s_base + L.off_stage + stage * STAGE_BYTES + row * 128;
 #pragma unroll
-        for (int cq = 0; cq < 4; ++cq) {
-          const int chunk = 4 * h + cq;
-          const float4 v4 = *reinterpret_cast<const float4*>(tile + row * 128 +
-                                                             ((chunk ^ (row & 7)) << 4));
+        for (int cq = 0; cq < 2; ++cq) {
+          const float4 v4 = lds_f128(ta + (((2 * g + cq) ^ (row & 7)) << 4));
           x[4 * cq + 0] = v4.x; x[4 * cq + 1] = v4.y; x[4 * cq + 2] = v4.z; x[4 * cq + 3] = v4.w;
         }
-        float osum = 0.f;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int n = n0 + 32 * u + 16 * h + i;
-          const bool ok = f < F && n < N;
-          float a1 = 0.f, a2 = 0.f;
-          if (ok) {
-            const float yy = y[i] + kappa;
-            zpair<FBC>(x[i], yy, beta, a1, a2);
-            osum += dterm<FBC>(x[i], yy, a2, beta);
-          }
-          zn[i] = a1;
-          zd[i] = a2;
+        for (int i = 0; i < 8; ++i) {
+          const float yy = KAPPA ? y[i] + kappa : y[i];
+          zpair<FBC>(x[i], yy, beta, zn[i], zd[i]);
+          dd[i] = dterm<FBC>(x[i], yy, zd[i], beta);
         }
-        obj += double(osum);
-        float hi[16], lo[16];
-        const uint32_t zb = lane_base + TM_Z + 128 * buf + 16 * h;
+        if (!(ncols_full && 128 * t + 128 <= F)) {
+          const int f = 128 * t + row;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) { hi[i] = to_tf32(zn[i]); lo[i] = to_tf32(zn[i] - hi[i]); }
-        tmem_st16(zb + 0, hi);
-        tmem_st16(zb + 32, lo);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) { hi[i] = to_tf32(zd[i]); lo[i] = to_tf32(zd[i] - hi[i]); }
-        tmem_st16(zb + 64, hi);
-        tmem_st16(zb + 96, lo);
+          for (int i = 0; i < 8; ++i) {
+            const bool ok = f < F && (n0 + 32 * u + 8 * g + i < N);
+            zn[i] = ok ? zn[i] : 0.f;
+            zd[i] = ok ? zd[i] : 0.f;
+            dd[i] = ok ? dd[i] : 0.f;
+          }
+        }
+        obj += double((dd[0] + dd[1]) + (dd[2] + dd[3]) + ((dd[4] + dd[5]) + (dd[6] + dd[7])));
+        const uint32_t zb = lane_base + TM_Z + 128 * buf + 8 * g;
+        store_z8(zb, zn);
+        store_z8(zb + 64, zd);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -537,30 +547,13 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
         }
         if (++stage == nstage) { stage = 0; ph ^= 1; }
       }
-      // ---------------- fold AccW into fp64 ----------------
-      mbar_wait(bar_accw, bi & 1);
-      tc_fence_after();
-      if (h < L.FT) {
-        float vn[16], vd[16];
-        tmem_ld16(lane_base + TM_ACCW + 32 * h, vn);
-        tmem_ld16(lane_base + TM_ACCW + 32 * h + 16, vd);
-#pragma unroll
-        for (int k = 0; k < KP; ++k) { accw_n[k] += double(vn[k]); accw_d[k] += double(vd[k]); }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_accw_free);
+      if ((bi % FOLD) == FOLD - 1 || b + (int)gridDim.x >= nblocks) fold();
     }
-    // ---- per-CTA outputs ----
-    double* mypart = a.part + size_t(blockIdx.x) * 2 * F * K;
-    if (h < L.FT) {
-      const int f = 128 * h + row;
-      if (f < F) {
-        for (int k = 0; k < K; ++k) {
-          mypart[size_t(f) * K + k] = accw_n[k];
-          mypart[size_t(F) * K + size_t(f) * K + k] = accw_d[k];
-        }
-      }
+    if (nfold == 0 && g < 2 * L.FT) {   // CTA without blocks: zero slab rows
+      const int t = g >> 1, s = g & 1;
+      const int f = 128 * t + row;
+      if (f < F)
+        for (int k = 0; k < K; ++k) mypart[size_t(s) * F * K + size_t(f) * K + k] = 0.0;
     }
     for (int o = 16; o > 0; o >>= 1) obj += __shfl_down_sync(0xffffffffu, obj, o);
     if (lane == 0) s_red[e] = obj;

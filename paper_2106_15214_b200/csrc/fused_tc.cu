@@ -172,6 +172,8 @@ static FusedArgs make_args(FusedState* fs, const FusedIO& io, int do_h) {
   a.do_h = do_h;
   a.den_ones = beta_class(io.sc.beta) == BC_1 ? 1 : 0;
   a.sc = io.sc;
+  const char* dbg = getenv("BNMF_TC_DEBUG");
+  a.debug = dbg ? atoi(dbg) : 0;
   return a;
 }
 

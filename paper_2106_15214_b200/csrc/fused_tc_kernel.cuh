@@ -45,8 +45,8 @@ constexpr uint32_t STAGE_BYTES = 32 * 128 * 4;
 // TMEM columns
 constexpr uint32_t TM_ACCW = 0;    // tile t: num at 32t, den at 32t+16
 constexpr uint32_t TM_ACCH = 64;   // num 64..79, den 80..95
-constexpr uint32_t TM_D = 96;      // D[buf] at 96 + 32 buf
-constexpr uint32_t TM_Z = 160;     // Z[buf] at 160 + 128 buf: num_hi, num_lo, den_hi, den_lo (32 each)
+constexpr uint32_t TM_D = 96;      // D[i] at 96 + 32 i, i < 3 (triple buffered)
+constexpr uint32_t TM_Z = 192;     // Z[b] at 192 + 128 b: num_hi, num_lo, den_hi, den_lo (32 each)
 
 // beta class of the fused TC epilogue (adds the beta = 1.5 fast form)
 enum { FBC_GEN = 0, FBC_0 = 1, FBC_1 = 2, FBC_2 = 3, FBC_15 = 4 };
@@ -127,27 +127,30 @@ __device__ __forceinline__ uint64_t dplus(uint64_t d, uint32_t off) { return d +
 // D (+)= A * B^T over K = 16 in 3xTF32: (hi,hi) + (hi,lo) + (lo,hi), 2 k-steps
 // each; A and B K-major core-tiled (LBO 128, SBO 512).
 __device__ __forceinline__ void issue_big(uint32_t dcol, uint64_t a_hi, uint64_t a_lo,
-                                          uint64_t b_hi, uint64_t b_lo, uint32_t idesc) {
-  mma_ss_elect(dcol, a_hi, b_hi, idesc, 0u);
-  mma_ss_elect(dcol, dplus(a_hi, 256), dplus(b_hi, 256), idesc, 1u);
-  mma_ss_elect(dcol, a_hi, b_lo, idesc, 1u);
-  mma_ss_elect(dcol, dplus(a_hi, 256), dplus(b_lo, 256), idesc, 1u);
-  mma_ss_elect(dcol, a_lo, b_hi, idesc, 1u);
-  mma_ss_elect(dcol, dplus(a_lo, 256), dplus(b_hi, 256), idesc, 1u);
+                                          uint64_t b_hi, uint64_t b_lo, uint32_t idesc,
+                                          int dbg = 0) {
+  if (dbg == 2) return;
+  mma_ss(dcol, a_hi, b_hi, idesc, 0u);
+  mma_ss(dcol, dplus(a_hi, 256), dplus(b_hi, 256), idesc, 1u);
+  mma_ss(dcol, a_hi, b_lo, idesc, 1u);
+  mma_ss(dcol, dplus(a_hi, 256), dplus(b_lo, 256), idesc, 1u);
+  mma_ss(dcol, a_lo, b_hi, idesc, 1u);
+  mma_ss(dcol, dplus(a_lo, 256), dplus(b_hi, 256), idesc, 1u);
 }
 
 // D (+)= Z * B over a 32-wide K slab: Z (hi/lo) in TMEM columns, B K-major
 // [16 x K]; 3xTF32, 4 k-steps each.
 __device__ __forceinline__ void issue_side(uint32_t dcol, uint32_t z_hi, uint32_t z_lo,
                                            uint64_t b_hi, uint64_t b_lo, uint32_t idesc,
-                                           bool fresh) {
+                                           bool fresh, int dbg = 0) {
+  if (dbg == 2) return;
 #pragma unroll
   for (int s = 0; s < 4; ++s)
-    mma_ts_elect(dcol, z_hi + 8 * s, dplus(b_hi, 256 * s), idesc, (fresh && s == 0) ? 0u : 1u);
+    mma_ts(dcol, z_hi + 8 * s, dplus(b_hi, 256 * s), idesc, (fresh && s == 0) ? 0u : 1u);
 #pragma unroll
-  for (int s = 0; s < 4; ++s) mma_ts_elect(dcol, z_hi + 8 * s, dplus(b_lo, 256 * s), idesc, 1u);
+  for (int s = 0; s < 4; ++s) mma_ts(dcol, z_hi + 8 * s, dplus(b_lo, 256 * s), idesc, 1u);
 #pragma unroll
-  for (int s = 0; s < 4; ++s) mma_ts_elect(dcol, z_lo + 8 * s, dplus(b_hi, 256 * s), idesc, 1u);
+  for (int s = 0; s < 4; ++s) mma_ts(dcol, z_lo + 8 * s, dplus(b_hi, 256 * s), idesc, 1u);
 }
 
 // store 8 Z values (hi/lo split) at TMEM columns col (hi) and col + 32 (lo)
@@ -175,14 +178,16 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.off_bar);
   uint64_t* bar_full = bars;                 // [nstage]
   uint64_t* bar_empty = bars + 8;            // [nstage]
-  uint64_t* bar_dfull = bars + 16;           // [2]
-  uint64_t* bar_zfull = bars + 18;           // [2]
-  uint64_t* bar_hp = bars + 20;
-  uint64_t* bar_hn = bars + 21;
-  uint64_t* bar_acch = bars + 22;
-  uint64_t* bar_accw = bars + 23;
-  uint64_t* bar_accw_free = bars + 24;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 26);
+  uint64_t* bar_dfull = bars + 16;           // [3]
+  uint64_t* bar_zfull = bars + 19;           // [2]
+  uint64_t* bar_zempty = bars + 21;          // [2]
+  uint64_t* bar_hp = bars + 23;
+  uint64_t* bar_hn = bars + 24;
+  uint64_t* bar_acch = bars + 25;
+  uint64_t* bar_accw = bars + 26;
+  uint64_t* bar_accw_free = bars + 27;
+  uint64_t* bar_wdone = bars + 28;           // all W-side MMAs of a block retired
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 29);
   __shared__ double s_red[NEPI];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -204,15 +209,17 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
       mbar_init(&bar_full[s], 1);
       mbar_init(&bar_empty[s], NEPI);
     }
+    for (int b = 0; b < 3; ++b) mbar_init(&bar_dfull[b], 1);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&bar_dfull[b], 1);
       mbar_init(&bar_zfull[b], NEPI);
+      mbar_init(&bar_zempty[b], 1);
     }
     mbar_init(bar_hp, NEPI);
     mbar_init(bar_hn, NEPI);
     mbar_init(bar_acch, 1);
     mbar_init(bar_accw, 1);
     mbar_init(bar_accw_free, NEPI);
+    mbar_init(bar_wdone, 1);
     mbar_fence_init();
   }
   if (warp == 0 && lane == 0) {
@@ -271,6 +278,10 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
     }
   } else if (warp == 1) {
     // ======================= MMA issuer (warp-uniform) ======================
+    // Sub-tiles are numbered c = bi * SB + s (s < SH: H phase, else W phase).
+    // D(c) is issued up to two sub-tiles ahead of the side MMAs of c, into
+    // one of three D buffers; the side MMAs of c wait for Z(c) from the
+    // epilogue and release the Z buffer through zempty.
     const uint32_t id_big = idesc_tf32(128, 32, 0, 0);
     const uint32_t id_side = idesc_tf32(128, 16, 0, 0);
     const uint64_t d_wa = sdesc(s_base + L.off_wa, 128, 512);
@@ -280,83 +291,79 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
     const uint64_t d_c1 = sdesc(s_base + L.off_c1, 128, uint32_t(L.FP) * 32);
     const uint64_t d_c2 = sdesc(s_base + L.off_c2, 128, uint32_t(L.FP) * 32);
     const uint64_t d_hnt = sdesc(s_base + L.off_hnt, 128, BN * 32);
-    uint32_t c = 0;       // sub-tile counter (D / Z double buffer)
-    int bi = 0;
-    int pending = -1;     // W sub-tile of the previous block still to issue
-    bool pend_fold = false;
-    // W side of sub-tile (cc, w): AccW[t] += Z * H~_p[u] (num and den)
-    auto side_w = [&](uint32_t cc, int w, bool fresh) {
-      const uint32_t zb = tmem + TM_Z + 128 * (cc & 1);
-      const int t = w >> 2, u = w & 3;
-      const uint64_t bh = dplus(d_hnt, u * 1024);
-      const uint64_t bl = dplus(bh, hb);
-      issue_side(tmem + TM_ACCW + 32 * t, zb, zb + 32, bh, bl, id_side, fresh && u == 0);
-      issue_side(tmem + TM_ACCW + 32 * t + 16, zb + 64, zb + 96, bh, bl, id_side, fresh && u == 0);
-    };
-    // H side of sub-tile (cc, j): AccH += ZT * chi[j]
-    auto side_h = [&](uint32_t cc, int j) {
-      const uint32_t zb = tmem + TM_Z + 128 * (cc & 1);
-      const uint64_t b1 = dplus(d_c1, j * 1024);
-      issue_side(tmem + TM_ACCH, zb, zb + 32, b1, dplus(b1, wb), id_side, j == 0);
-      if (!den_ones) {
-        const uint64_t b2 = dplus(d_c2, j * 1024);
-        issue_side(tmem + TM_ACCH + 16, zb + 64, zb + 96, b2, dplus(b2, wb), id_side, j == 0);
-      }
-    };
-    auto wait_z = [&](uint32_t cc) {
-      mbar_wait(&bar_zfull[cc & 1], (cc >> 1) & 1);
-      tc_fence_after();
-    };
-    auto flush_pending = [&]() {
-      if (pending >= 0) {
-        wait_z(c - 1);
-        side_w(c - 1, pending, false);
-        if (pend_fold) mma_commit_elect(bar_accw);
-        pending = -1;
-      }
-    };
-    for (int b = blockIdx.x; b < nblocks; b += gridDim.x, ++bi) {
-      const bool fresh = (bi % FOLD) == 0;
-      if (do_h) {
-        mbar_wait(bar_hp, bi & 1);
-        tc_fence_after();
-        for (int j = 0; j < L.SH; ++j, ++c) {
-          issue_big(tmem + TM_D + 32 * (c & 1), d_hp, dplus(d_hp, hb), dplus(d_wa, j * 2048),
-                    dplus(d_wa, j * 2048 + wb), id_big);
-          mma_commit_elect(&bar_dfull[c & 1]);
-          if (j > 0) {
-            wait_z(c - 1);
-            side_h(c - 1, j - 1);
-          } else {
-            flush_pending();
-          }
-        }
-        wait_z(c - 1);
-        side_h(c - 1, L.SH - 1);
-        mma_commit_elect(bar_acch);
-      } else {
-        flush_pending();
-      }
-      mbar_wait(bar_hn, bi & 1);
-      tc_fence_after();
-      for (int w = 0; w < L.SW; ++w, ++c) {
-        const int t = w >> 2, u = w & 3;
-        issue_big(tmem + TM_D + 32 * (c & 1), dplus(d_wt, t * 8192), dplus(d_wt, t * 8192 + wb),
-                  dplus(d_hn, u * 2048), dplus(d_hn, u * 2048 + hb), id_big);
-        mma_commit_elect(&bar_dfull[c & 1]);
-        if (w > 0) {
-          wait_z(c - 1);
-          if (w == 1 && fresh && bi > 0) {
-            mbar_wait(bar_accw_free, ((bi / FOLD) - 1) & 1);
+    const int SHh = do_h ? L.SH : 0;
+    const int SB = SHh + L.SW;
+    const int nb_cta = blockIdx.x < nblocks ? (nblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int total = a.debug == 3 ? 0 : nb_cta * SB;
+    int nd = 0;
+    for (int cs = 0; cs < total; ++cs) {
+      // ---- issue D's ahead (three buffers) ----
+      while (nd < total && nd <= cs + 2) {
+        const int bi_d = nd / SB, s_d = nd - bi_d * SB;
+        const uint32_t dcol = tmem + TM_D + 32 * (nd % 3);
+        if (s_d < SHh) {
+          if (s_d == 0) {
+            mbar_wait(bar_hp, bi_d & 1);
             tc_fence_after();
           }
-          side_w(c - 1, w - 1, fresh);
+          if (elect_one())
+            issue_big(dcol, d_hp, dplus(d_hp, hb), dplus(d_wa, s_d * 2048),
+                      dplus(d_wa, s_d * 2048 + wb), id_big, a.debug);
+        } else {
+          const int w = s_d - SHh, t = w >> 2, u = w & 3;
+          if (w == 0) {
+            // H~_p of this block needs every side MMA issued before it (the
+            // epilogue's H update waits for them): no run-ahead past here
+            if (cs < bi_d * SB + SHh) break;
+            mbar_wait(bar_hn, bi_d & 1);
+            tc_fence_after();
+          }
+          if (elect_one())
+            issue_big(dcol, dplus(d_wt, t * 8192), dplus(d_wt, t * 8192 + wb),
+                      dplus(d_hn, u * 2048), dplus(d_hn, u * 2048 + hb), id_big, a.debug);
         }
+        if (elect_one()) mma_commit(&bar_dfull[nd % 3]);
+        __syncwarp();
+        ++nd;
       }
-      pending = L.SW - 1;
-      pend_fold = (bi % FOLD) == FOLD - 1 || b + (int)gridDim.x >= nblocks;
+      // ---- side MMAs of sub-tile cs ----
+      mbar_wait(&bar_zfull[cs & 1], (cs >> 1) & 1);
+      tc_fence_after();
+      const int bi = cs / SB, s_c = cs - bi * SB;
+      const uint32_t zb = tmem + TM_Z + 128 * (cs & 1);
+      if (s_c < SHh) {
+        const uint64_t b1 = dplus(d_c1, s_c * 1024);
+        const uint64_t b2 = dplus(d_c2, s_c * 1024);
+        if (elect_one()) {
+          issue_side(tmem + TM_ACCH, zb, zb + 32, b1, dplus(b1, wb), id_side, s_c == 0, a.debug);
+          if (!den_ones)
+            issue_side(tmem + TM_ACCH + 16, zb + 64, zb + 96, b2, dplus(b2, wb), id_side, s_c == 0,
+                       a.debug);
+          mma_commit(&bar_zempty[cs & 1]);
+          if (s_c == SHh - 1) mma_commit(bar_acch);
+        }
+        __syncwarp();
+      } else {
+        const int w = s_c - SHh, t = w >> 2, u = w & 3;
+        const bool fresh = (bi % FOLD) == 0 && u == 0;
+        if (w == 0 && (bi % FOLD) == 0 && bi > 0) {
+          mbar_wait(bar_accw_free, ((bi / FOLD) - 1) & 1);
+          tc_fence_after();
+        }
+        const uint64_t bh = dplus(d_hnt, u * 1024);
+        const uint64_t bl = dplus(bh, hb);
+        const bool last_w = w == L.SW - 1;
+        const bool fold_end = (bi % FOLD) == FOLD - 1 || bi == nb_cta - 1;
+        if (elect_one()) {
+          issue_side(tmem + TM_ACCW + 32 * t, zb, zb + 32, bh, bl, id_side, fresh, a.debug);
+          issue_side(tmem + TM_ACCW + 32 * t + 16, zb + 64, zb + 96, bh, bl, id_side, fresh, a.debug);
+          mma_commit(&bar_zempty[cs & 1]);
+          if (last_w && fold_end) mma_commit(bar_accw);
+          if (last_w) mma_commit(bar_wdone);
+        }
+        __syncwarp();
+      }
     }
-    flush_pending();
     __syncwarp();
   } else {
     // ======================= epilogue =======================================
@@ -405,6 +412,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
     };
     // add the TMEM W sums of the last FOLD blocks into the fp64 slab
     auto fold = [&]() {
+      if (a.debug == 3) { ++nfold; return; }
       mbar_wait(bar_accw, nfold & 1);
       tc_fence_after();
       if (g < 2 * L.FT) {
@@ -438,18 +446,25 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
       if (do_h) {
         // ---------------- H phase ----------------
         for (int j = 0; j < L.SH; ++j, ++c) {
-          const uint32_t buf = c & 1;
-          mbar_wait(&bar_dfull[buf], (c >> 1) & 1);
+          const uint32_t buf = c & 1, dbuf = c % 3;
+          const bool nomma = a.debug == 3;
+          if (!nomma) mbar_wait(&bar_dfull[dbuf], (c / 3) & 1);
           mbar_wait(&bar_full[stage], ph);
           tc_fence_after();
           float y[8], x[8], zn[8], zd[8];
-          tmem_ld8(lane_base + TM_D + 32 * buf + 8 * g, y);
+          if (!nomma) tmem_ld8(lane_base + TM_D + 32 * dbuf + 8 * g, y);
+          else for (int i = 0; i < 8; ++i) y[i] = 1.f;
           const uint32_t xa = s_base + L.off_stage + stage * STAGE_BYTES + (8 * g * 128 + row) * 4;
+          if (a.debug == 1) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) x[i] = lds_f32(xa + i * 512);
+            for (int i = 0; i < 8; ++i) { zn[i] = y[i]; zd[i] = y[i]; }
+          } else {
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            zpair<FBC>(x[i], KAPPA ? y[i] + kappa : y[i], beta, zn[i], zd[i]);
+            for (int i = 0; i < 8; ++i) x[i] = lds_f32(xa + i * 512);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              zpair<FBC>(x[i], KAPPA ? y[i] + kappa : y[i], beta, zn[i], zd[i]);
+          }
           if (!(ncols_full && 32 * j + 32 <= F)) {
             const bool nok = n0 + row < N;
 #pragma unroll
@@ -460,8 +475,16 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
             }
           }
           const uint32_t zb = lane_base + TM_Z + 128 * buf + 8 * g;
-          store_z8(zb, zn);
-          if (!den_ones) store_z8(zb + 64, zd);
+          if (c >= 2 && !nomma) {   // side MMAs of c-2 released this Z buffer
+            mbar_wait(&bar_zempty[buf], ((c - 2) >> 1) & 1);
+            tc_fence_after();
+          }
+          if (!nomma) {
+            store_z8(zb, zn);
+            if (!den_ones) store_z8(zb + 64, zd);
+          } else if (zn[0] == 12345.f && zd[1] == 1.f) {
+            obj += 1.0;
+          }
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
@@ -472,11 +495,15 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
           if (++stage == nstage) { stage = 0; ph ^= 1; }
         }
         // ---------------- H update ----------------
-        mbar_wait(bar_acch, bi & 1);
-        tc_fence_after();
         float nv[4], dv[4], hv[4];
-        tmem_ld4(lane_base + TM_ACCH + 4 * g, nv);
-        if (!den_ones) tmem_ld4(lane_base + TM_ACCH + 16 + 4 * g, dv);
+        if (a.debug != 3) {
+          mbar_wait(bar_acch, bi & 1);
+          tc_fence_after();
+          tmem_ld4(lane_base + TM_ACCH + 4 * g, nv);
+          if (!den_ones) tmem_ld4(lane_base + TM_ACCH + 16 + 4 * g, dv);
+        } else {
+          for (int i = 0; i < 4; ++i) { nv[i] = 1.f; dv[i] = 1.f; }
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int k = 4 * g + i;
@@ -489,8 +516,10 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
           hv[i] = v;
         }
         tc_fence_before();
+        if (bi > 0 && a.debug != 3) mbar_wait(bar_wdone, (bi - 1) & 1);   // W MMAs of bi-1 read H~ smem
         store_hnew(n0, hv);
       } else {
+        if (bi > 0 && a.debug != 3) mbar_wait(bar_wdone, (bi - 1) & 1);
         store_hnew(n0, hprev);
       }
       fence_async_smem();
@@ -505,24 +534,31 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
       }
       // ---------------- W phase ----------------
       for (int w = 0; w < L.SW; ++w, ++c) {
-        const uint32_t buf = c & 1;
+        const uint32_t buf = c & 1, dbuf = c % 3;
         const int t = w >> 2, u = w & 3;
-        mbar_wait(&bar_dfull[buf], (c >> 1) & 1);
+        const bool nomma = a.debug == 3;
+        if (!nomma) mbar_wait(&bar_dfull[dbuf], (c / 3) & 1);
         mbar_wait(&bar_full[stage], ph);
         tc_fence_after();
         float y[8], x[8], zn[8], zd[8], dd[8];
-        tmem_ld8(lane_base + TM_D + 32 * buf + 8 * g, y);
+        if (!nomma) tmem_ld8(lane_base + TM_D + 32 * dbuf + 8 * g, y);
+        else for (int i = 0; i < 8; ++i) y[i] = 1.f;
         const uint32_t ta = s_base + L.off_stage + stage * STAGE_BYTES + row * 128;
+        if (a.debug == 1) {
 #pragma unroll
-        for (int cq = 0; cq < 2; ++cq) {
-          const float4 v4 = lds_f128(ta + (((2 * g + cq) ^ (row & 7)) << 4));
-          x[4 * cq + 0] = v4.x; x[4 * cq + 1] = v4.y; x[4 * cq + 2] = v4.z; x[4 * cq + 3] = v4.w;
-        }
+          for (int i = 0; i < 8; ++i) { zn[i] = y[i]; zd[i] = y[i]; dd[i] = 0.f; }
+        } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float yy = KAPPA ? y[i] + kappa : y[i];
-          zpair<FBC>(x[i], yy, beta, zn[i], zd[i]);
-          dd[i] = dterm<FBC>(x[i], yy, zd[i], beta);
+          for (int cq = 0; cq < 2; ++cq) {
+            const float4 v4 = lds_f128(ta + (((2 * g + cq) ^ (row & 7)) << 4));
+            x[4 * cq + 0] = v4.x; x[4 * cq + 1] = v4.y; x[4 * cq + 2] = v4.z; x[4 * cq + 3] = v4.w;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float yy = KAPPA ? y[i] + kappa : y[i];
+            zpair<FBC>(x[i], yy, beta, zn[i], zd[i]);
+            dd[i] = dterm<FBC>(x[i], yy, zd[i], beta);
+          }
         }
         if (!(ncols_full && 128 * t + 128 <= F)) {
           const int f = 128 * t + row;
@@ -536,8 +572,16 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
         }
         obj += double((dd[0] + dd[1]) + (dd[2] + dd[3]) + ((dd[4] + dd[5]) + (dd[6] + dd[7])));
         const uint32_t zb = lane_base + TM_Z + 128 * buf + 8 * g;
-        store_z8(zb, zn);
-        store_z8(zb + 64, zd);
+        if (c >= 2 && !nomma) {
+          mbar_wait(&bar_zempty[buf], ((c - 2) >> 1) & 1);
+          tc_fence_after();
+        }
+        if (!nomma) {
+          store_z8(zb, zn);
+          store_z8(zb + 64, zd);
+        } else if (zn[0] == 12345.f && zd[1] == 1.f) {
+          obj += 1.0;
+        }
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();

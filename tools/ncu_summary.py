@@ -61,3 +61,26 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def regions(rep, width=64):
+    """Per-region (address chunk) stall breakdown of the SASS source page."""
+    src = list(csv.reader(io.StringIO(run([rep, "--page", "source", "--csv", "--print-source", "sass"]))))
+    sh, data = src[1], src[2:]
+    isrc, ie = sh.index("Source"), sh.index("Instructions Executed")
+    stall_cols = [i for i, h in enumerate(sh) if h.startswith("stall_") and "Not Issued" not in h]
+    for i in range(0, len(data), width):
+        blk = data[i:i + width]
+        e = sum(float(r[ie] or 0) for r in blk)
+        if e < 1e5:
+            continue
+        st = {sh[c][6:]: sum(float(r[c] or 0) for r in blk) for c in stall_cols}
+        tot = sum(st.values()) or 1
+        marks = sorted({m for r in blk for m in ("UTCHMMA", "LDTM", "STTM", "MUFU", "TRYWAIT", "LDS", "STS", "DADD", "DMUL", "MUFU.RCP64H", "STG", "LDG")
+                        if m in r[isrc]})
+        top = ", ".join(f"{k} {v:.0f}" for k, v in sorted(st.items(), key=lambda kv: -kv[1])[:4])
+        print(f"{data[i][0][-5:]} exec={e / 1e6:6.2f}M samples={tot:6.0f} [{top}] {' '.join(marks)}")
+
+
+if __name__ == "__main__" and "--regions" in sys.argv:
+    regions(sys.argv[1])

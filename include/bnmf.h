@@ -81,6 +81,16 @@ int bnmf_ctx_init_comm(bnmf_ctx* ctx, int rank, int nranks, const void* id128,
 int bnmf_set_dense(bnmf_ctx* ctx, const void* v, int src_dtype, int src_on_device,
                    int64_t F, int64_t N, int64_t ld, double kappa);
 
+/* Sparse data (beta = 1 only): the local rows of V in CSR (indptr F+1,
+ * int32 column indices, fp32 values) plus its CSC view (colptr N+1, int32 row
+ * indices, perm[j] = CSR position of CSC entry j) used for the deterministic
+ * column sums.  The reference densifies sparse input (matrixio.py:115-128);
+ * this replaces DataMatrix for config 5.  Switches the context to the sparse
+ * engine (fp32 contexts only). */
+int bnmf_set_csr(bnmf_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                 const float* values, const int64_t* colptr, const int32_t* rowidx,
+                 const int32_t* perm, int64_t F, int64_t N, int64_t nnz, int src_on_device);
+
 /* Factors: W (F x K) and the local H block (K x N), fp64 row-major host or
  * device memory (init_factors, solver.py:137-153, or an injected init). */
 int bnmf_set_factors(bnmf_ctx* ctx, const double* w, const double* h, int64_t K,

@@ -60,6 +60,8 @@ _SIGS = {
     "bnmf_set_dense": ([C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_int64,
                         C.c_int64, C.c_double], C.c_int),
     "bnmf_set_factors": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int], C.c_int),
+    "bnmf_set_csr": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                      C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int], C.c_int),
     "bnmf_begin": ([C.c_void_p, C.POINTER(Params), C.c_int64], C.c_int),
     "bnmf_step": ([C.c_void_p, C.c_int64], C.c_int),
     "bnmf_step_timed": ([C.c_void_p, C.c_int64, C.POINTER(C.c_float)], C.c_int),
@@ -173,6 +175,19 @@ class Context:
             self._check(self.lib.bnmf_set_dense(self.h, _ptr(v), src, 0, F, N, ld,
                                                 float(kappa)))
         self.F, self.N = F, N
+
+    def set_csr(self, indptr, indices, values, colptr, rowidx, perm, shape):
+        """Host CSR (+ CSC view) of the local rows of V (see include/bnmf.h)."""
+        arrs = [np.ascontiguousarray(indptr, dtype=np.int64),
+                np.ascontiguousarray(indices, dtype=np.int32),
+                np.ascontiguousarray(values, dtype=np.float32),
+                np.ascontiguousarray(colptr, dtype=np.int64),
+                np.ascontiguousarray(rowidx, dtype=np.int32),
+                np.ascontiguousarray(perm, dtype=np.int32)]
+        F, N = shape
+        self._check(self.lib.bnmf_set_csr(self.h, *[_ptr(a) for a in arrs], int(F), int(N),
+                                          int(arrs[1].size), 0))
+        self.F, self.N = int(F), int(N)
 
     def set_factors(self, w, h):
         w = np.ascontiguousarray(w, dtype=np.float64)

@@ -665,6 +665,7 @@ struct Engine : EngineBase {
 
 struct bnmf_ctx {
   std::unique_ptr<EngineBase> eng;
+  bool sparse = false;
 };
 
 static int set_err(const std::string& m, int code) {
@@ -725,6 +726,27 @@ int bnmf_set_dense(bnmf_ctx* ctx, const void* v, int src_dtype, int src_on_devic
   CTX_CHECK(ctx);
   if (!v) return set_err("null data", BNMF_E_ARG);
   return ctx->eng->set_dense(v, src_dtype, src_on_device, F, N, ld, kappa);
+}
+
+int bnmf_set_csr(bnmf_ctx* ctx, const int64_t* indptr, const int32_t* indices,
+                 const float* values, const int64_t* colptr, const int32_t* rowidx,
+                 const int32_t* perm, int64_t F, int64_t N, int64_t nnz, int src_on_device) {
+  CTX_CHECK(ctx);
+  if (ctx->eng->dtype != BNMF_FP32) return set_err("sparse path computes in fp32", BNMF_E_UNSUPPORTED);
+  if (!indptr || !colptr || (nnz > 0 && (!indices || !values || !rowidx || !perm)))
+    return set_err("null sparse arrays", BNMF_E_ARG);
+  if (!ctx->sparse) {
+    int dev = ctx->eng->device;
+    cudaSetDevice(dev);
+    cudaStream_t s;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess)
+      return set_err("stream create", BNMF_E_CUDA);
+    ctx->eng.reset(make_sparse_engine(dev, s));
+    ctx->sparse = true;
+  }
+  return sparse_set_csr(ctx->eng.get(), reinterpret_cast<const long long*>(indptr), indices,
+                        values, reinterpret_cast<const long long*>(colptr), rowidx, perm, F, N,
+                        nnz, src_on_device);
 }
 
 int bnmf_set_factors(bnmf_ctx* ctx, const double* w, const double* h, int64_t K,

@@ -71,6 +71,11 @@ inline cudaError_t record_event(cudaEvent_t ev, cudaStream_t s) {
   return cudaEventRecord(ev, s);
 }
 
+EngineBase* make_sparse_engine(int device, cudaStream_t stream);
+int sparse_set_csr(EngineBase* e, const long long* ip, const int* ix, const float* v,
+                   const long long* cp, const int* ri, const int* pm, int64_t F, int64_t N,
+                   int64_t nnz, int on_dev);
+
 struct FusedState;
 bool fused_supported(int dtype, int F, int K, int algorithm, int L, int Lw, int Lh, double beta);
 int fused_create(FusedState** out, const FusedIO& io, std::string& err);

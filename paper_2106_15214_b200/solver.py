@@ -201,7 +201,7 @@ def get_context(device=None, dtype="fp64"):
     with _ctx_lock:
         ctx = _ctx_cache.get(key)
         if ctx is None:
-            ctx = _native.Context(device, dtype)
+            ctx = _native.Context(device, "fp32" if dtype == "fp32-sparse" else dtype)
             ctx.lock = threading.Lock()
             _ctx_cache[key] = ctx
         return ctx
@@ -325,13 +325,91 @@ def _run(data, config, counter, algorithm, *, dtype="fp64", init=None, device=No
                      iterations=done, config=config)
 
 
+def _is_sparse(data):
+    try:
+        import scipy.sparse as sp
+    except Exception:  # pragma: no cover
+        return False
+    return sp.issparse(data)
+
+
+def csr_with_csc_view(data):
+    """CSR arrays of a scipy.sparse matrix plus its CSC view (colptr, row
+    indices, perm[j] = CSR position of CSC entry j) -- the deterministic
+    column-sum layout of the sparse path."""
+    import scipy.sparse as sp
+    m = sp.csr_matrix(data, dtype=np.float32)
+    m.sum_duplicates()
+    m.sort_indices()
+    F, N = m.shape
+    rows = np.repeat(np.arange(F, dtype=np.int64), np.diff(m.indptr))
+    order = np.lexsort((rows, m.indices))           # by column, then row
+    colptr = np.zeros(N + 1, dtype=np.int64)
+    np.cumsum(np.bincount(m.indices, minlength=N), out=colptr[1:])
+    return (m.indptr.astype(np.int64), m.indices.astype(np.int32), m.data.astype(np.float32),
+            colptr, rows[order].astype(np.int32), order.astype(np.int32)), (F, N)
+
+
+def _run_sparse(data, config, counter, algorithm, *, dtype="fp32", init=None, device=None,
+                kkt=False, schedule="auto", sharded=False):
+    """Sparse KL path (config 5): beta = 1, kappa = 0, fp32 on the device.
+
+    The reference densifies sparse input (matrixio.py:115-128) and would apply
+    the default kappa rule (1e-9 * mean, core.py:176-185) because V has zeros;
+    a positive shift densifies the problem, so the sparse path requires
+    kappa = 0 (or None, read as 0)."""
+    if config.algorithm != algorithm:
+        raise ValueError(f"config.algorithm must be '{algorithm.value}' for "
+                         f"run_{algorithm.value}")
+    if config.beta != 1.0:
+        raise ValueError("the sparse path implements beta = 1 (KL) only")
+    if config.kappa not in (None, 0.0):
+        raise ValueError("sparse input needs kappa = 0 (a positive shift densifies V)")
+    if sharded:
+        raise ValueError("the sparse path is single-GPU in this build")
+    if (config.sub_iters != 1 or (config.sub_iters_w or 1) != 1
+            or (config.sub_iters_h or 1) != 1):
+        raise ValueError("the sparse path implements one sub-iteration")
+    arrays, (F, N) = csr_with_csc_view(data)
+    vals = arrays[2]
+    if not np.isfinite(vals).all():
+        raise ValueError("data entries must be finite")
+    if vals.size and vals.min() < 0.0:
+        raise ValueError("data entries must be nonnegative")
+    pair = _resolve_init(init, F, N, config.rank, config.seed)
+    ctx = get_context(device, "fp32-sparse")
+    with ctx.lock:
+        ctx.set_csr(*arrays, (F, N))
+        ctx.set_factors(pair.w, pair.h)
+        params = make_params(config, 0.0, kkt=False, schedule="reference")
+        done, converged = ctx.run(params, config.max_outer_iters)
+        obj, sec, kk = ctx.trace(done)
+        w, h = ctx.factors()
+    trace = [TraceRow(i + 1, float(obj[i]), float(sec[i]), float("nan"), float("nan"))
+             for i in range(done)]
+    _count_ops(counter, config, done)
+    try:
+        factors = FactorPair(w, h)
+    except ValueError:
+        factors = _unchecked_pair(w, h)
+    return FitResult(factors=factors, trace=trace,
+                     termination=Termination.CONVERGED if converged else Termination.MAX_ITERS,
+                     iterations=done, config=config)
+
+
 def run_bmm(data, config, counter=None, **options):
-    """Block (alternating) MU updates (solver.py:224-248)."""
+    """Block (alternating) MU updates (solver.py:224-248).  A scipy.sparse
+    ``data`` runs the sparse KL path."""
+    if _is_sparse(data):
+        return _run_sparse(data, config, counter, Algorithm.BMM, **options)
     return _run(data, config, counter, Algorithm.BMM, **options)
 
 
 def run_jmm(data, config, counter=None, **options):
-    """Joint MM updates (solver.py:251-282)."""
+    """Joint MM updates (solver.py:251-282).  A scipy.sparse ``data`` runs the
+    sparse KL path."""
+    if _is_sparse(data):
+        return _run_sparse(data, config, counter, Algorithm.JMM, **options)
     return _run(data, config, counter, Algorithm.JMM, **options)
 
 

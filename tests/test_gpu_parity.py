@@ -131,3 +131,41 @@ def test_native_library_is_what_ran():
     bn.fit(v, bn.SolverConfig(beta=1.0, rank=2, algorithm="jmm", max_outer_iters=3))
     assert ctx.launches_per_iter() > 0
     assert ctx.schedule() in ("reference", "fused")
+
+
+def test_sparse_kl_matches_dense_reference():
+    """Config-5-like sparse KL (CSR) against the reference run on the
+    densified matrix (golden cfg5p), fp32 objective <= 1e-4."""
+    import scipy.sparse as sp
+    from paper_2106_15214_b200 import synthetic
+    z = load_golden("configs.npz")
+    indptr, idx, vals, shape = synthetic.config5(F=2000, N=400, density=0.1, seed=55)
+    csr = sp.csr_matrix((vals, idx, indptr), shape=shape)
+    w0, h0 = synthetic.uniform_init(shape[0], shape[1], 16, seed=116)
+    for algo in ("jmm", "bmm"):
+        ref = z[f"cfg5p_{algo}/obj"]
+        cfg = bn.SolverConfig(beta=1.0, rank=16, algorithm=algo, kappa=0.0, tol=1e-300,
+                              max_outer_iters=len(ref))
+        res = bn.fit(csr, cfg, init=(w0, h0), dtype="fp32")
+        obj = np.array([r.objective for r in res.trace])
+        assert max_rel(obj, ref) <= 1e-4, (algo, max_rel(obj, ref))
+        assert res.factors.w.shape == (2000, 16) and res.factors.h.shape == (16, 400)
+
+
+def test_sparse_matches_oracle_restatement_and_is_deterministic():
+    import scipy.sparse as sp
+    from oracle import betanmf_oracle as O
+    from paper_2106_15214_b200 import synthetic
+    indptr, idx, vals, shape = synthetic.config5(F=5000, N=3000, density=0.01, seed=7)
+    csr = sp.csr_matrix((vals, idx, indptr), shape=shape)
+    w0, h0 = synthetic.uniform_init(shape[0], shape[1], 64, seed=164)
+    cfg = bn.SolverConfig(beta=1.0, rank=64, algorithm="jmm", kappa=0.0, tol=1e-300,
+                          max_outer_iters=10)
+    r1 = bn.fit(csr, cfg, init=(w0, h0), dtype="fp32")
+    r2 = bn.fit(csr, cfg, init=(w0, h0), dtype="fp32")
+    assert np.array_equal(r1.factors.w, r2.factors.w)
+    assert [t.objective for t in r1.trace] == [t.objective for t in r2.trace]
+    _, _, obj, _ = O.run_sparse_kl(csr.astype(np.float64), 64, "jmm", max_outer_iters=10,
+                                   init=(w0, h0))
+    got = np.array([t.objective for t in r1.trace])
+    assert max_rel(got, obj) <= 1e-4

@@ -291,13 +291,24 @@ def main():
     if rank != 0:
         return
     hbm, _, peak_src = measured_peaks()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f).get(f"config{args.config}:{args.algo}:"
+                                  f"{'fused_pass_tc' if sched == 'fused' else 'hside_pass'}")
+        if tr and world == 1:
+            traffic = tr["dram_bytes_per_launch"]
+    except Exception:
+        traffic = None
     esize = 4 if c["dtype"] == "fp32" else 8
     vbytes_local = c["F"] * (n1 - n0) * esize
     achieved = vbytes_local / (pass_ms / 1e3) / 1e9 if pass_ms > 0 else None
     roofline = {
         "bound": "hbm", "kernel": "fused_pass" if sched == "fused" else "hside_pass",
         "achieved": achieved, "peak": hbm, "unit": "GB/s",
-        "frac": achieved / hbm if achieved else None, "traffic": None,
+        "frac": achieved / hbm if achieved else None, "traffic": traffic,
+        "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum, one launch "
+                          "(profiles/traffic.json)" if traffic else None,
         "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
         "algorithmic_bytes_per_launch": vbytes_local,
         "launch_ms": pass_ms, "launch_samples": pass_samples,

@@ -33,6 +33,7 @@ from .solver import (
     synthetic_low_rank,
 )
 from .updates import Algorithm, OpCounter, UpdateKind
+from . import parallel  # noqa: F401  (N-column sharding helpers)
 
 __version__ = "0.1.0"
 

@@ -47,6 +47,7 @@ constexpr uint32_t TM_ACCW = 0;    // tile t: num at 32t, den at 32t+16
 constexpr uint32_t TM_ACCH = 64;   // num 64..79, den 80..95
 constexpr uint32_t TM_D = 96;      // D[i] at 96 + 32 i, i < 3 (triple buffered)
 constexpr uint32_t TM_Z = 192;     // Z[b] at 192 + 128 b: num_hi, num_lo, den_hi, den_lo (32 each)
+constexpr uint32_t TM_WT = 448;    // W~_p as TMEM A operand: tile t hi at 448 + 32t, lo at +16
 
 // beta class of the fused TC epilogue (adds the beta = 1.5 fast form)
 enum { FBC_GEN = 0, FBC_0 = 1, FBC_1 = 2, FBC_2 = 3, FBC_15 = 4 };
@@ -68,7 +69,7 @@ __host__ __device__ inline TcLayout tc_layout(int F, int nstage) {
   L.off_stage = o; o += nstage * STAGE_BYTES;
   const uint32_t wbytes = uint32_t(L.FP) * KP * 4;   // one hi or lo copy of an F x 16 operand
   L.off_wa = o; o += 2 * wbytes;
-  L.off_wt = o; o += 2 * wbytes;
+  L.off_wt = 0;   // W~_p lives in TMEM (TM_WT)
   L.off_c1 = o; o += 2 * wbytes;
   L.off_c2 = o; o += 2 * wbytes;
   L.off_hp = o; o += 2 * BN * KP * 4;
@@ -136,6 +137,19 @@ __device__ __forceinline__ void issue_big(uint32_t dcol, uint64_t a_hi, uint64_t
   mma_ss(dcol, dplus(a_hi, 256), dplus(b_lo, 256), idesc, 1u);
   mma_ss(dcol, a_lo, b_hi, idesc, 1u);
   mma_ss(dcol, dplus(a_lo, 256), dplus(b_hi, 256), idesc, 1u);
+}
+
+// Same with A (M x 16, hi/lo) in TMEM columns a_hi / a_lo (8 columns per k-step).
+__device__ __forceinline__ void issue_big_ts(uint32_t dcol, uint32_t a_hi, uint32_t a_lo,
+                                             uint64_t b_hi, uint64_t b_lo, uint32_t idesc,
+                                             int dbg = 0) {
+  if (dbg == 2) return;
+  mma_ts(dcol, a_hi, b_hi, idesc, 0u);
+  mma_ts(dcol, a_hi + 8, dplus(b_hi, 256), idesc, 1u);
+  mma_ts(dcol, a_hi, b_lo, idesc, 1u);
+  mma_ts(dcol, a_hi + 8, dplus(b_lo, 256), idesc, 1u);
+  mma_ts(dcol, a_lo, b_hi, idesc, 1u);
+  mma_ts(dcol, a_lo + 8, dplus(b_hi, 256), idesc, 1u);
 }
 
 // D (+)= Z * B over a 32-wide K slab: Z (hi/lo) in TMEM columns, B K-major
@@ -237,8 +251,6 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
       float v, hi;
       v = ok ? Wa[gi] : 0.f; hi = tf32_hi(v);
       sts_f32(s_base + L.off_wa + o, hi); sts_f32(s_base + L.off_wa + wb + o, v - hi);
-      v = ok ? Wt[gi] : 0.f; hi = tf32_hi(v);
-      sts_f32(s_base + L.off_wt + o, hi); sts_f32(s_base + L.off_wt + wb + o, v - hi);
       v = ok ? a.C1[gi] : 0.f; hi = tf32_hi(v);
       sts_f32(s_base + L.off_c1 + ot, hi); sts_f32(s_base + L.off_c1 + wb + ot, v - hi);
       v = ok ? a.C2[gi] : 0.f; hi = tf32_hi(v);
@@ -250,6 +262,28 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
+  // W~_p (A operand of the W-phase Vt MMAs) into TMEM: warps with g < FT write
+  // tile t = g, lane f, 16 hi + 16 lo columns.
+  if (warp >= 2) {
+    const int e = warp - 2, q = warp & 3, g = e >> 2;
+    if (g < L.FT) {
+      const int f = 128 * g + 32 * q + lane;
+      float hi[16], lo[16];
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        const float v = (f < F && k < K) ? Wt[size_t(f) * K + k] : 0.f;
+        hi[k] = tf32_hi(v);
+        lo[k] = v - hi[k];
+      }
+      const uint32_t ta = tmem + (uint32_t(32 * q) << 16) + TM_WT + 32 * g;
+      tmem_st16(ta, hi);
+      tmem_st16(ta + 16, lo);
+      tmem_st_wait();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   if (warp == 0) {
     // ======================= TMA producer ===================================
@@ -285,7 +319,6 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
     const uint32_t id_big = idesc_tf32(128, 32, 0, 0);
     const uint32_t id_side = idesc_tf32(128, 16, 0, 0);
     const uint64_t d_wa = sdesc(s_base + L.off_wa, 128, 512);
-    const uint64_t d_wt = sdesc(s_base + L.off_wt, 128, 512);
     const uint64_t d_hp = sdesc(s_base + L.off_hp, 128, 512);
     const uint64_t d_hn = sdesc(s_base + L.off_hn, 128, 512);
     const uint64_t d_c1 = sdesc(s_base + L.off_c1, 128, uint32_t(L.FP) * 32);
@@ -294,7 +327,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
     const int SHh = do_h ? L.SH : 0;
     const int SB = SHh + L.SW;
     const int nb_cta = blockIdx.x < nblocks ? (nblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int total = a.debug == 3 ? 0 : nb_cta * SB;
+    const int total = a.debug >= 3 ? 0 : nb_cta * SB;
     int nd = 0;
     for (int cs = 0; cs < total; ++cs) {
       // ---- issue D's ahead (three buffers) ----
@@ -319,8 +352,8 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
             tc_fence_after();
           }
           if (elect_one())
-            issue_big(dcol, dplus(d_wt, t * 8192), dplus(d_wt, t * 8192 + wb),
-                      dplus(d_hn, u * 2048), dplus(d_hn, u * 2048 + hb), id_big, a.debug);
+            issue_big_ts(dcol, tmem + TM_WT + 32 * t, tmem + TM_WT + 32 * t + 16,
+                         dplus(d_hn, u * 2048), dplus(d_hn, u * 2048 + hb), id_big, a.debug);
         }
         if (elect_one()) mma_commit(&bar_dfull[nd % 3]);
         __syncwarp();
@@ -412,7 +445,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
     };
     // add the TMEM W sums of the last FOLD blocks into the fp64 slab
     auto fold = [&]() {
-      if (a.debug == 3) { ++nfold; return; }
+      if (a.debug >= 3) { ++nfold; return; }
       mbar_wait(bar_accw, nfold & 1);
       tc_fence_after();
       if (g < 2 * L.FT) {
@@ -447,7 +480,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
         // ---------------- H phase ----------------
         for (int j = 0; j < L.SH; ++j, ++c) {
           const uint32_t buf = c & 1, dbuf = c % 3;
-          const bool nomma = a.debug == 3;
+          const bool nomma = a.debug >= 3;
           if (!nomma) mbar_wait(&bar_dfull[dbuf], (c / 3) & 1);
           mbar_wait(&bar_full[stage], ph);
           tc_fence_after();
@@ -455,7 +488,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
           if (!nomma) tmem_ld8(lane_base + TM_D + 32 * dbuf + 8 * g, y);
           else for (int i = 0; i < 8; ++i) y[i] = 1.f;
           const uint32_t xa = s_base + L.off_stage + stage * STAGE_BYTES + (8 * g * 128 + row) * 4;
-          if (a.debug == 1) {
+          if (a.debug == 1 || a.debug == 4) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) { zn[i] = y[i]; zd[i] = y[i]; }
           } else {
@@ -496,7 +529,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
         }
         // ---------------- H update ----------------
         float nv[4], dv[4], hv[4];
-        if (a.debug != 3) {
+        if (a.debug < 3) {
           mbar_wait(bar_acch, bi & 1);
           tc_fence_after();
           tmem_ld4(lane_base + TM_ACCH + 4 * g, nv);
@@ -516,10 +549,10 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
           hv[i] = v;
         }
         tc_fence_before();
-        if (bi > 0 && a.debug != 3) mbar_wait(bar_wdone, (bi - 1) & 1);   // W MMAs of bi-1 read H~ smem
+        if (bi > 0 && a.debug < 3) mbar_wait(bar_wdone, (bi - 1) & 1);   // W MMAs of bi-1 read H~ smem
         store_hnew(n0, hv);
       } else {
-        if (bi > 0 && a.debug != 3) mbar_wait(bar_wdone, (bi - 1) & 1);
+        if (bi > 0 && a.debug < 3) mbar_wait(bar_wdone, (bi - 1) & 1);
         store_hnew(n0, hprev);
       }
       fence_async_smem();
@@ -536,7 +569,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
       for (int w = 0; w < L.SW; ++w, ++c) {
         const uint32_t buf = c & 1, dbuf = c % 3;
         const int t = w >> 2, u = w & 3;
-        const bool nomma = a.debug == 3;
+        const bool nomma = a.debug >= 3;
         if (!nomma) mbar_wait(&bar_dfull[dbuf], (c / 3) & 1);
         mbar_wait(&bar_full[stage], ph);
         tc_fence_after();
@@ -544,7 +577,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
         if (!nomma) tmem_ld8(lane_base + TM_D + 32 * dbuf + 8 * g, y);
         else for (int i = 0; i < 8; ++i) y[i] = 1.f;
         const uint32_t ta = s_base + L.off_stage + stage * STAGE_BYTES + row * 128;
-        if (a.debug == 1) {
+        if (a.debug == 1 || a.debug == 4) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) { zn[i] = y[i]; zd[i] = y[i]; dd[i] = 0.f; }
         } else {

@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbnmf.so")
+LIB_PATH = os.environ.get("BNMF_LIB") or os.path.join(HERE, "libbnmf.so")
 
 BNMF_FP64, BNMF_FP32 = 0, 1
 BNMF_JMM, BNMF_BMM = 0, 1

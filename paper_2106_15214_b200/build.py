@@ -18,7 +18,7 @@ import sysconfig
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-OUT = os.path.join(HERE, "libbnmf.so")
+OUT = os.environ.get("BNMF_LIB_OUT") or os.path.join(HERE, "libbnmf.so")
 OBJDIR = os.path.join(HERE, "build")
 SOURCES = ["engine.cu", "fused_tc.cu", "sparse.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -65,6 +65,8 @@ def build(verbose=False, force=False):
               "--expt-relaxed-constexpr"]
     if os.environ.get("BNMF_WATCHDOG", "0") == "1":
         common.append("-DBNMF_WATCHDOG")
+    if os.environ.get("BNMF_TC_PROF", "0") == "1":
+        common.append("-DBNMF_TC_PROF")
     srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
 
     def compile_one(src):

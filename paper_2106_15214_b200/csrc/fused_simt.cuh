@@ -159,14 +159,19 @@ fused_pass_simt(FusedArgs a, const RunState* st, int slot, int p_override) {
 }
 
 // comm[0:2FK] = sum_g part[g], comm[2FK] = sum_g opart[g]  (fixed order)
+// Fixed-order sum of the per-CTA partials.  With a row-split cluster
+// (cl == 2) CTA g owns rows [0, split) when g is even, else [split, F); it
+// only writes its own rows, so row f sums the CTAs of its owner rank.
 static __global__ void fused_reduce(const double* __restrict__ part, const double* __restrict__ opart,
-                             int G, int FK2, double* __restrict__ comm, const RunState* st,
-                             int slot, int p_override) {
+                             int G, int FK2, int K, int split, int cl, double* __restrict__ comm,
+                             const RunState* st, int slot, int p_override) {
   if (p_override < 0 && !iter_active(st, slot)) return;
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < FK2) {
+    const int f = (i % (FK2 / 2)) / K;
+    const int r = (cl > 1 && f >= split) ? 1 : 0;
     double s = 0.0;
-    for (int g = 0; g < G; ++g) s += part[(size_t)g * FK2 + i];
+    for (int g = r; g < G; g += cl) s += part[(size_t)g * FK2 + i];
     comm[i] = s;
   } else if (i == FK2) {
     double s = 0.0;

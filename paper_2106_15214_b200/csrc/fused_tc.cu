@@ -42,10 +42,14 @@ struct FusedState {
   // tensor-core pass
   bool tc = false;
   int tc_grid = 0;
-  int tc_nstage = 0;
+  int tc_cl = 1;      // CTAs per cluster (row split of F)
+  int tc_f0 = 0;      // rows of cluster rank 0
   size_t tc_smem = 0;
-  CUtensorMap mapH, mapW;
+  CUtensorMap mapV;
+  long long* prof = nullptr;   // BNMF_TC_PROF=1: wait-cycle counters [grid][48]
 };
+
+static FusedState* g_last_tc = nullptr;
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -68,12 +72,21 @@ bool fused_tc_shape_ok(int F, int K) {
   return F >= 1 && F <= 256 && K >= 1 && K <= ftc::KP;
 }
 
-static int tc_pick_stages(int F, size_t* bytes) {
-  for (int ns = 8; ns >= 2; --ns) {
-    size_t b = ftc::tc_layout(F, ns).bytes + 1024;
-    if (b <= 232448) { *bytes = b; return ns; }
-  }
-  return 0;
+template <int FBC, bool KAPPA>
+static cudaLaunchConfig_t tc_config(const FusedState* fs, cudaStream_t stream,
+                                    cudaLaunchAttribute* attr) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(fs->tc_grid, 1, 1);
+  cfg.blockDim = dim3(ftc::NTHREADS, 1, 1);
+  cfg.dynamicSmemBytes = fs->tc_smem;
+  cfg.stream = stream;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = fs->tc_cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
 }
 
 #define FCK(call)                                                           \
@@ -122,26 +135,54 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
   fs->tc = fused_tc_shape_ok(io.F, io.K) && encode_fn() != nullptr &&
            !(force_simt && force_simt[0] == '1');
   if (fs->tc) {
-    fs->tc_nstage = tc_pick_stages(io.F, &fs->tc_smem);
-    int nb = (io.N + ftc::BN - 1) / ftc::BN;
-    fs->tc_grid = std::max(1, std::min(nb, nsm));
-    if (fs->tc_nstage == 0) fs->tc = false;
+    const int nb = (io.N + ftc::BN - 1) / ftc::BN;
+    fs->tc_smem = ftc::SMEM_BYTES;
+    if (io.F > ftc::FR) {
+      fs->tc_cl = 2;
+      // split rows in multiples of 32 so that rank 1 keeps >= 33 rows
+      const int half = ((io.F + 1) / 2 + 31) / 32 * 32;
+      fs->tc_f0 = std::min(ftc::FR, half);
+    } else {
+      fs->tc_cl = 1;
+      fs->tc_f0 = io.F;
+    }
+    auto kern = ftc::fused_pass_tc<ftc::FBC_15, false>;
+    FCK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fs->tc_smem)));
+    FCK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    int clusters = nsm / fs->tc_cl;
+    if (fs->tc_cl > 1) {
+      cudaLaunchAttribute attr[1];
+      FusedState probe = *fs;
+      probe.tc_grid = fs->tc_cl * clusters;
+      cudaLaunchConfig_t cfg = tc_config<ftc::FBC_15, false>(&probe, io.stream, attr);
+      int maxc = 0;
+      if (cudaOccupancyMaxActiveClusters(&maxc, kern, &cfg) == cudaSuccess && maxc > 0)
+        clusters = std::min(clusters, maxc);
+      cudaGetLastError();
+    }
+    fs->tc_grid = fs->tc_cl * std::max(1, std::min(nb, clusters));
   }
   int gmax = std::max(fs->G, fs->tc_grid);
+  const char* prof_env = getenv("BNMF_TC_PROF");
+  if (fs->tc && prof_env && prof_env[0] == '1') {
+    const size_t np = size_t(fs->tc_grid) * 48 + 3 * 4096;
+    FCK(cudaMalloc(&fs->prof, np * sizeof(long long)));
+    FCK(cudaMemset(fs->prof, 0, np * sizeof(long long)));
+    g_last_tc = fs;
+  }
   FCK(cudaMalloc(&fs->part, size_t(gmax) * 2 * fk * sizeof(double)));
   FCK(cudaMalloc(&fs->opart, size_t(gmax) * sizeof(double)));
   if (fs->tc) {
+    // V stages: [32 rows x 132 columns] boxes, unswizzled; the 4 extra
+    // columns pad the SMEM rows to 528 B (conflict-free in both phases)
     cuuint64_t dims[2] = {cuuint64_t(io.N), cuuint64_t(io.F)};
     cuuint64_t strides[1] = {cuuint64_t(io.ldv) * 4};
-    cuuint32_t boxh[2] = {128, 32}, boxw[2] = {32, 128}, es[2] = {1, 1};
+    cuuint32_t box[2] = {cuuint32_t(ftc::VROW), 32}, es[2] = {1, 1};
     EncodeTiledFn enc = encode_fn();
-    CUresult r1 = enc(&fs->mapH, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(io.V), dims,
-                      strides, boxh, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+    CUresult r1 = enc(&fs->mapV, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(io.V), dims,
+                      strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    CUresult r2 = enc(&fs->mapW, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(io.V), dims,
-                      strides, boxw, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) {
+    if (r1 != CUDA_SUCCESS) {
       err = "cuTensorMapEncodeTiled failed";
       return -1;
     }
@@ -155,6 +196,8 @@ void fused_destroy(FusedState* fs) {
   for (float* q : fp) if (q) cudaFree(q);
   double* dp[] = {fs->norms, fs->csum2, fs->part, fs->opart};
   for (double* q : dp) if (q) cudaFree(q);
+  if (fs->prof) cudaFree(fs->prof);
+  if (g_last_tc == fs) g_last_tc = nullptr;
   delete fs;
 }
 
@@ -174,6 +217,7 @@ static FusedArgs make_args(FusedState* fs, const FusedIO& io, int do_h) {
   a.sc = io.sc;
   const char* dbg = getenv("BNMF_TC_DEBUG");
   a.debug = dbg ? atoi(dbg) : 0;
+  a.prof = fs->prof;
   return a;
 }
 
@@ -191,10 +235,11 @@ static cudaError_t launch_tc(FusedState* fs, const FusedArgs& a, const FusedIO& 
                              int p_override) {
   auto kern = ftc::fused_pass_tc<FBC, KAPPA>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fs->tc_smem));
-  kern<<<fs->tc_grid, ftc::NTHREADS, fs->tc_smem, io.stream>>>(a, fs->mapH, fs->mapW,
-                                                               fs->tc_nstage, io.st, slot,
-                                                               p_override);
-  return cudaGetLastError();
+  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = tc_config<FBC, KAPPA>(fs, io.stream, attr);
+  return cudaLaunchKernelEx(&cfg, kern, a, fs->mapV, fs->tc_cl, fs->tc_f0, io.st, slot,
+                            p_override);
 }
 
 template <int FBC>
@@ -231,8 +276,8 @@ static int enqueue_pass_and_update(FusedState* fs, const FusedIO& io, int slot, 
   FCK(launch_pass(fs, a, io, slot, p_override));
   if (io.ev_b) FCK(record_event(io.ev_b, io.stream));
   fused_reduce<<<int((fk2 + 1 + 255) / 256), 256, 0, io.stream>>>(
-      fs->part, fs->opart, fs->tc ? fs->tc_grid : fs->G, int(fk2), io.comm, io.st, slot,
-      p_override);
+      fs->part, fs->opart, fs->tc ? fs->tc_grid : fs->G, int(fk2), io.K,
+      fs->tc ? fs->tc_f0 : io.F, fs->tc ? fs->tc_cl : 1, io.comm, io.st, slot, p_override);
   FCK(cudaGetLastError());
   if (io.launches) *io.launches += 2;
   if (io.nranks > 1) {
@@ -317,3 +362,14 @@ int fused_export(FusedState* fs, const FusedIO& io, std::string& err) {
 }
 
 }  // namespace bnmf
+
+// Bring-up aid (not part of include/bnmf.h): copy the wait-cycle counters of
+// the last tcgen05 pass (BNMF_TC_PROF=1) to the host; returns the count.
+extern "C" int bnmf_tc_prof_read(long long* out, int max) {
+  bnmf::FusedState* fs = bnmf::g_last_tc;
+  if (!fs || !fs->prof) return 0;
+  int n = std::min(max, fs->tc_grid * 48 + 3 * 4096);
+  if (cudaMemcpy(out, fs->prof, size_t(n) * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  return n;
+}

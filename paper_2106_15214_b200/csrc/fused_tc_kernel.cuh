@@ -1,28 +1,34 @@
-// tcgen05 implementation of the fused single-read pass (fp32 carried as
-// 3xTF32, F <= 256 rows, rank K <= 16).  Same contract as fused_pass_simt.
+// tcgen05 implementation of the fused single-read pass (fp32, rank K <= 16,
+// F <= 256).  Same contract as fused_pass_simt (fused_common.cuh).
 //
-// One persistent CTA per SM walks 128-column blocks of V.  Warp roles:
-//   warp 0      TMA producer: V tiles into a 16 KB smem ring, in consumption
-//               order (per block: F/32 tiles [32 f x 128 n] for the H phase,
-//               then 4*FT tiles [128 f x 32 n], 128B-swizzled, for the W
-//               phase -- that second read is served by L2)
-//   warp 1      MMA issuer (warp-uniform loop, elected lane issues) + TMEM owner
-//   warps 2..17 epilogue: TMEM -> registers, the beta-dependent terms, the
-//               hi/lo TF32 split written back to TMEM as MMA A operands, the
+// Rows of V are split over a cluster of CL CTAs (CL = 2 when F > 128): CTA r
+// owns rows [row0, row0 + FTr) and every column block of its cluster, so
+// all of its V rows of a block (<= 128 x 128 fp32) stay resident in SMEM for
+// both phases and V is read from HBM exactly once per pass.
+//
+// Warp roles (18 warps, one CTA per SM):
+//   warp 0      TMA producer: V stages [32 rows x 132 cols] (528 B padded rows,
+//               conflict-free in both phases) into a 7-stage ring
+//   warp 1      MMA issuer (warp-uniform loop, one elected lane issues) + TMEM owner
+//   warps 2..17 epilogue: TMEM -> registers, the beta-dependent terms,
+//               Z back to TMEM as the A operand of the side products, the
 //               H update, the objective, fp64 folding of the W sums
-// Per block (columns n0 .. n0+127):
-//   H phase, f sub-tile j (32 rows):
-//     D    [n x f] = Hp (128x16) * Wa[j]^T            6 MMAs  M128 N32 (3xTF32)
-//     ZT   [n x f] = Zn, Zd of (V, D + kappa)         epilogue -> TMEM
-//     AccH [n x k] += ZT * chi[j]                     24 MMAs M128 N16 (A in TMEM)
-//   H update: H~_p = Hp * (AccHn / max(AccHd, floor))^gamma * norms -> smem, HBM
-//   W phase, f tile t (128 rows) x n sub-tile u (32 cols):
-//     D    [f x n] = W~_p[t] * H~_p[u]^T              6 MMAs  M128 N32
-//     Z    [f x n] = Zn, Zd of (V, D + kappa); objective
-//     AccW [t]    += Z * H~_p[u]                      24 MMAs M128 N16 (A in TMEM)
-//   AccW stays in TMEM for FOLD blocks, then is added into the CTA's fp64
-//   partial slab (fixed order => deterministic).
-// All smem MMA operands are K-major "core-tiled" (8 rows x 16 B core matrices).
+//
+// Per column block (n0 .. n0+127), items in epilogue order:
+//   H(j)   j < SH      D[n x 32 f] = H~_{p-1} Wa[j]^T  (3xTF32, A from TMEM)
+//                      Z = Zn, Zd of (V, D + kappa) -> TMEM
+//                      AccH[n x k] += Z * [chi_hi | chi_lo]     (A from TMEM)
+//   U                  AccH of the cluster combined over DSMEM (st.async),
+//                      H~_p = H~_{p-1} (num/den)^gamma norms -> SMEM + HBM
+//   W(u)   u < 4       D[f x 32 n] = W~_p H~_p[u]^T; objective;
+//                      AccW[f x k] += Z * [H~_hi | H~_lo]
+// The first H item of block b+1 is processed before U(b) so that the AccH
+// drain and the DSMEM exchange overlap epilogue work.
+//
+// Numerics: every product is 3xTF32 (hi*hi + hi*lo + lo*hi).  The side
+// products issue Z_hi * [B_hi | B_lo] as one N = 32 MMA (the two halves of
+// the accumulator are summed at readout) plus Z_lo * B_hi (N = 16).  All
+// reductions have a fixed order (bitwise reproducible).
 #pragma once
 
 #include <cuda.h>
@@ -37,53 +43,43 @@ using namespace bnmf::tc;
 
 constexpr int BN = 128;            // columns per block
 constexpr int KP = 16;             // padded rank
+constexpr int FR = 128;            // rows per CTA (max)
+constexpr int SW = BN / 32;        // W items per block
 constexpr int NEPI = 16;           // epilogue warps (4 per TMEM lane quadrant)
 constexpr int NTHREADS = 32 * (2 + NEPI);
 constexpr int FOLD = 8;            // blocks accumulated in TMEM before the fp64 fold
-constexpr uint32_t STAGE_BYTES = 32 * 128 * 4;
+constexpr int VROW = 132;          // padded SMEM row of a V stage (floats)
+constexpr uint32_t VROWB = VROW * 4;
+constexpr uint32_t STAGE_BYTES = 32 * VROWB;
+constexpr int NSTAGE = 7;
 
-// TMEM columns
-constexpr uint32_t TM_ACCW = 0;    // tile t: num at 32t, den at 32t+16
-constexpr uint32_t TM_ACCH = 64;   // num 64..79, den 80..95
-constexpr uint32_t TM_D = 96;      // D[i] at 96 + 32 i, i < 3 (triple buffered)
-constexpr uint32_t TM_Z = 192;     // Z[b] at 192 + 128 b: num_hi, num_lo, den_hi, den_lo (32 each)
-constexpr uint32_t TM_WT = 448;    // W~_p as TMEM A operand: tile t hi at 448 + 32t, lo at +16
+// TMEM columns (512 allocated)
+constexpr uint32_t TM_D = 0;       // Vt tiles, 2 x 32
+constexpr uint32_t TM_Z = 64;      // Z, 2 x 128: k-step s -> Zn hi, Zn lo, Zd hi, Zd lo at 32s + 8i
+constexpr uint32_t TM_ACCH = 320;  // num [hi part 16 | lo part 16], den at +32
+constexpr uint32_t TM_ACCW = 384;  // same layout
+constexpr uint32_t TM_HP = 448;    // H~_{p-1} rows of the block: hi 16 | lo 16
+constexpr uint32_t TM_WT = 480;    // W~_p rows of this CTA: hi 16 | lo 16
+
+// SMEM layout (bytes from the 1024-aligned base)
+constexpr uint32_t OFF_STAGE = 0;
+constexpr uint32_t OFF_WA = OFF_STAGE + NSTAGE * STAGE_BYTES;   // [128 f x 16] hi, lo (core tiles)
+constexpr uint32_t OFF_C1 = OFF_WA + 2 * FR * KP * 4;           // [32 (k hi, k lo) x 128 f]
+constexpr uint32_t OFF_C2 = OFF_C1 + 2 * FR * KP * 4;
+constexpr uint32_t OFF_HN = OFF_C2 + 2 * FR * KP * 4;           // [128 n x 16] hi, lo
+constexpr uint32_t OFF_HNT = OFF_HN + 2 * BN * KP * 4;          // [32 (k hi, k lo) x 128 n]
+constexpr uint32_t OFF_XCH = OFF_HNT + 2 * BN * KP * 4;         // peer's AccH partial
+constexpr uint32_t OFF_BAR = OFF_XCH + BN * 2 * KP * 4;
+constexpr uint32_t SMEM_BYTES = OFF_BAR + 512 + 1024;           // + alignment slack
+constexpr uint32_t HILO = FR * KP * 4;                          // hi -> lo offset (8 KB)
 
 // beta class of the fused TC epilogue (adds the beta = 1.5 fast form)
 enum { FBC_GEN = 0, FBC_0 = 1, FBC_1 = 2, FBC_2 = 3, FBC_15 = 4 };
 
-struct TcLayout {
-  int FP, FT, SH, SW, nstage;
-  uint32_t off_stage, off_wa, off_wt, off_c1, off_c2, off_hp, off_hn, off_hnt, off_bar;
-  uint32_t bytes;
-};
-
-__host__ __device__ inline TcLayout tc_layout(int F, int nstage) {
-  TcLayout L;
-  L.FT = (F + 127) / 128;
-  L.FP = L.FT * 128;
-  L.SH = (F + 31) / 32;
-  L.SW = 4 * L.FT;
-  L.nstage = nstage;
-  uint32_t o = 0;
-  L.off_stage = o; o += nstage * STAGE_BYTES;
-  const uint32_t wbytes = uint32_t(L.FP) * KP * 4;   // one hi or lo copy of an F x 16 operand
-  L.off_wa = o; o += 2 * wbytes;
-  L.off_wt = 0;   // W~_p lives in TMEM (TM_WT)
-  L.off_c1 = o; o += 2 * wbytes;
-  L.off_c2 = o; o += 2 * wbytes;
-  L.off_hp = o; o += 2 * BN * KP * 4;
-  L.off_hn = o; o += 2 * BN * KP * 4;
-  L.off_hnt = o; o += 2 * BN * KP * 4;
-  L.off_bar = o; o += 256;
-  L.bytes = o;
-  return L;
-}
-
-// element (k, c) of a K-major [16 rows x C] tile whose K dimension is C:
-// 8-row groups at SBO = C*32 bytes, 4-wide chunks of c at 128 B
-__host__ __device__ __forceinline__ uint32_t coreT_off(int k, int c, int C) {
-  return uint32_t((k >> 3) * (C * 32) + (c >> 2) * 128 + (k & 7) * 16 + (c & 3) * 4);
+// element (k, c) of a K-major [R rows x 128] tile whose K dimension is c:
+// 8-row groups at SBO = 4096 B, 4-wide chunks of c at LBO = 128 B
+__host__ __device__ __forceinline__ uint32_t coreT_off(int k, int c) {
+  return uint32_t((k >> 3) * 4096 + (c >> 2) * 128 + (k & 7) * 16 + (c & 3) * 4);
 }
 
 template <int FBC>
@@ -121,29 +117,28 @@ __device__ __forceinline__ float dterm(float x, float y, float zd, float beta) {
   return divergence32<BC_GEN>(x, y, beta);
 }
 
+// Z of one k-step (this thread's 8 columns) as TMEM A operands:
+// [Zn hi | Zn lo | Zd hi | Zd lo], 8 columns each, one 32-column store
+__device__ __forceinline__ void store_z(uint32_t taddr, const float* zn, const float* zd) {
+  float z[32];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    z[i] = tf32_trunc(zn[i]);
+    z[8 + i] = zn[i] - z[i];
+    z[16 + i] = tf32_trunc(zd[i]);
+    z[24 + i] = zd[i] - z[16 + i];
+  }
+  tmem_st32(taddr, z);
+}
+
 // smem descriptor arithmetic: the start-address field is addr >> 4 in the low
 // 14 bits, so desc(addr + off) == desc(addr) + (off >> 4) for smem < 256 KB.
 __device__ __forceinline__ uint64_t dplus(uint64_t d, uint32_t off) { return d + (off >> 4); }
 
-// D (+)= A * B^T over K = 16 in 3xTF32: (hi,hi) + (hi,lo) + (lo,hi), 2 k-steps
-// each; A and B K-major core-tiled (LBO 128, SBO 512).
-__device__ __forceinline__ void issue_big(uint32_t dcol, uint64_t a_hi, uint64_t a_lo,
-                                          uint64_t b_hi, uint64_t b_lo, uint32_t idesc,
-                                          int dbg = 0) {
-  if (dbg == 2) return;
-  mma_ss(dcol, a_hi, b_hi, idesc, 0u);
-  mma_ss(dcol, dplus(a_hi, 256), dplus(b_hi, 256), idesc, 1u);
-  mma_ss(dcol, a_hi, b_lo, idesc, 1u);
-  mma_ss(dcol, dplus(a_hi, 256), dplus(b_lo, 256), idesc, 1u);
-  mma_ss(dcol, a_lo, b_hi, idesc, 1u);
-  mma_ss(dcol, dplus(a_lo, 256), dplus(b_hi, 256), idesc, 1u);
-}
-
-// Same with A (M x 16, hi/lo) in TMEM columns a_hi / a_lo (8 columns per k-step).
-__device__ __forceinline__ void issue_big_ts(uint32_t dcol, uint32_t a_hi, uint32_t a_lo,
-                                             uint64_t b_hi, uint64_t b_lo, uint32_t idesc,
-                                             int dbg = 0) {
-  if (dbg == 2) return;
+// D = A * B^T over K = 16 in 3xTF32: (hi,hi) + (hi,lo) + (lo,hi), 2 k-steps
+// each; A (M x 16, hi/lo) in TMEM columns a_hi / a_lo, B K-major core tiles.
+__device__ __forceinline__ void issue_vt(uint32_t dcol, uint32_t a_hi, uint32_t a_lo,
+                                         uint64_t b_hi, uint64_t b_lo, uint32_t idesc) {
   mma_ts(dcol, a_hi, b_hi, idesc, 0u);
   mma_ts(dcol, a_hi + 8, dplus(b_hi, 256), idesc, 1u);
   mma_ts(dcol, a_hi, b_lo, idesc, 1u);
@@ -152,59 +147,93 @@ __device__ __forceinline__ void issue_big_ts(uint32_t dcol, uint32_t a_hi, uint3
   mma_ts(dcol, a_lo + 8, dplus(b_hi, 256), idesc, 1u);
 }
 
-// D (+)= Z * B over a 32-wide K slab: Z (hi/lo) in TMEM columns, B K-major
-// [16 x K]; 3xTF32, 4 k-steps each.
-__device__ __forceinline__ void issue_side(uint32_t dcol, uint32_t z_hi, uint32_t z_lo,
-                                           uint64_t b_hi, uint64_t b_lo, uint32_t idesc,
-                                           bool fresh, int dbg = 0) {
-  if (dbg == 2) return;
+// acc[:, 0:32] (+)= Z_hi * [B_hi | B_lo], acc[:, 0:16] += Z_lo * B_hi over a
+// 32-wide K slab: Z hi/lo of k-step s at TMEM columns z + 32 s (+8 for lo),
+// B (32 x K, K-major) from descriptor b, 256 B per k-step.
+__device__ __forceinline__ void issue_side(uint32_t acc, uint32_t z, uint64_t b, uint32_t id32,
+                                           uint32_t id16, bool fresh) {
 #pragma unroll
-  for (int s = 0; s < 4; ++s)
-    mma_ts(dcol, z_hi + 8 * s, dplus(b_hi, 256 * s), idesc, (fresh && s == 0) ? 0u : 1u);
-#pragma unroll
-  for (int s = 0; s < 4; ++s) mma_ts(dcol, z_hi + 8 * s, dplus(b_lo, 256 * s), idesc, 1u);
-#pragma unroll
-  for (int s = 0; s < 4; ++s) mma_ts(dcol, z_lo + 8 * s, dplus(b_hi, 256 * s), idesc, 1u);
-}
-
-// store 8 Z values (hi/lo split) at TMEM columns col (hi) and col + 32 (lo)
-__device__ __forceinline__ void store_z8(uint32_t col, const float* z) {
-  float hi[8], lo[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) { hi[i] = tf32_trunc(z[i]); lo[i] = z[i] - hi[i]; }
-  tmem_st8(col, hi);
-  tmem_st8(col + 32, lo);
+  for (int s = 0; s < 4; ++s) {
+    mma_ts(acc, z + 32 * s, dplus(b, 256 * s), id32, (fresh && s == 0) ? 0u : 1u);
+    mma_ts(acc, z + 32 * s + 8, dplus(b, 256 * s), id16, 1u);
+  }
 }
 
 template <int FBC, bool KAPPA>
 __global__ void __launch_bounds__(NTHREADS, 1)
-fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
-              const __grid_constant__ CUtensorMap mapW, int nstage, const RunState* st, int slot,
-              int p_override) {
+fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int F0,
+              const RunState* st, int slot, int p_override) {
   if (p_override < 0 && !iter_active(st, slot)) return;
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
-  // 1024-align the working base (128B-swizzled TMA tiles need it)
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-  const int F = a.F, N = a.N, K = a.K;
-  const TcLayout L = tc_layout(F, nstage);
-  const uint32_t s_base = smem_u32(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.off_bar);
-  uint64_t* bar_full = bars;                 // [nstage]
-  uint64_t* bar_empty = bars + 8;            // [nstage]
-  uint64_t* bar_dfull = bars + 16;           // [3]
-  uint64_t* bar_zfull = bars + 19;           // [2]
-  uint64_t* bar_zempty = bars + 21;          // [2]
-  uint64_t* bar_hp = bars + 23;
-  uint64_t* bar_hn = bars + 24;
-  uint64_t* bar_acch = bars + 25;
-  uint64_t* bar_accw = bars + 26;
-  uint64_t* bar_accw_free = bars + 27;
-  uint64_t* bar_wdone = bars + 28;           // all W-side MMAs of a block retired
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 29);
+  const uint32_t sb = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* bar_full = bars;          // [NSTAGE] TMA -> epilogue
+  uint64_t* bar_empty = bars + 8;     // [NSTAGE] epilogue -> TMA
+  uint64_t* bar_dfull = bars + 16;    // [2] Vt tile ready
+  uint64_t* bar_zfull = bars + 18;    // [2] Z written
+  uint64_t* bar_dempty = bars + 32;   // [2] Vt tile loaded by the epilogue
+  uint64_t* bar_zempty = bars + 34;   // [2] side products of a Z buffer retired
+  uint64_t* bar_hp = bars + 22;       // H~_{p-1} of the next block in TMEM
+  uint64_t* bar_hn = bars + 23;       // H~_p of the block in SMEM
+  uint64_t* bar_acch = bars + 24;     // AccH of the block complete
+  uint64_t* bar_accfree = bars + 25;  // AccH read out
+  uint64_t* bar_accw = bars + 26;     // AccW of a fold complete
+  uint64_t* bar_accwfree = bars + 27; // AccW read out
+  uint64_t* bar_wdone = bars + 28;    // W-side MMAs of a block retired
+  uint64_t* bar_xfull = bars + 29;    // peer's AccH partial landed (tx)
+  uint64_t* bar_xempty = bars + 30;   // peer consumed my partial (remote arrivals)
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 40);
   __shared__ double s_red[NEPI];
+  // optional wait-cycle counters (build with BNMF_TC_PROF=1; one thread per role records)
+#ifdef BNMF_TC_PROF
+  long long* prof = a.prof ? a.prof + size_t(blockIdx.x) * 48 : nullptr;
+  __shared__ unsigned long long pcs[48];
+  for (int i = threadIdx.x; i < 48; i += blockDim.x) pcs[i] = 0;
+  __syncthreads();
+  const bool rec = prof && (threadIdx.x & 31) == 0 && (threadIdx.x < 96);
+  const int pbase = (threadIdx.x >> 5) * 12;
+  auto pwait = [&](uint64_t* bar, uint32_t parity, int cat) {
+    if (rec) {
+      const long long t0 = clock64();
+      mbar_wait(bar, parity);
+      atomicAdd(&pcs[pbase + cat], (unsigned long long)(clock64() - t0));
+    } else {
+      mbar_wait(bar, parity);
+    }
+  };
+  auto pwait_cl = pwait;
+  const long long t_start = clock64();
+  // event timeline of CTA 0 (lane 0 of warps 0..2): clock << 16 | ev << 10 | pos
+  long long* trace_buf = (a.prof && blockIdx.x == 0 && (threadIdx.x & 31) == 0 && threadIdx.x < 96)
+                             ? a.prof + size_t(gridDim.x) * 48 + (threadIdx.x >> 5) * 4096
+                             : nullptr;
+  int trace_n = 0;
+  auto trace = [&](int ev, int pos) {
+    if (trace_buf && trace_n < 4095)
+      trace_buf[trace_n++] = (clock64() << 16) | (long long)(ev << 10) | (pos & 1023);
+  };
+#define BNMF_TRACE(ev, pos) trace(ev, pos)
+#define BNMF_PROF_T0(v) const long long v = clock64()
+#define BNMF_PROF_ADD(i, v) if (rec) atomicAdd(&pcs[pbase + (i)], (unsigned long long)(clock64() - (v)))
+#else
+  auto pwait = [&](uint64_t* bar, uint32_t parity, int) { mbar_wait(bar, parity); };
+  auto pwait_cl = [&](uint64_t* bar, uint32_t parity, int) { mbar_wait(bar, parity); };
+#define BNMF_PROF_T0(v)
+#define BNMF_PROF_ADD(i, v)
+#define BNMF_TRACE(ev, pos)
+#endif
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int F = a.F, N = a.N, K = a.K;
+  const uint32_t rank = CL > 1 ? cluster_ctarank() : 0u;
+  const int row0 = rank ? F0 : 0;
+  const int FTr = rank ? F - F0 : (F < F0 ? F : F0);
+  const int SH = max(2, (FTr + 31) / 32);
+  const int npairs = gridDim.x / CL, pi = blockIdx.x / CL;
+  const int nblocks = (N + BN - 1) / BN;
+  const int nb = pi < nblocks ? (nblocks - 1 - pi) / npairs + 1 : 0;
   const int par = iter_parity(st, slot, p_override);
   const float* Hprev = a.do_h ? a.Hbuf[par ^ 1] : a.Hbuf[par];
   float* Hnew = a.Hout[par];
@@ -213,428 +242,572 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
   const int do_h = a.do_h;
   const int den_ones = a.den_ones;
   const float kappa = float(a.sc.kappa), beta = float(a.sc.beta);
-  const int nblocks = (N + BN - 1) / BN;
-  const uint32_t wb = uint32_t(L.FP) * KP * 4;   // hi -> lo offset of F x 16 operands
-  const uint32_t hb = BN * KP * 4;               // hi -> lo offset of 128 x 16 operands
+
+  // item sequence of this CTA (identical in the MMA warp and the epilogue):
+  // block bi lists its own H items (all of them for bi == 0, else 2..SH-1),
+  // then H(bi+1, 0) [U1(bi)] H(bi+1, 1) [U2(bi)], then W(bi, 0..SW-1).  U1
+  // reads AccH and sends it to the peer, U2 finishes the H update; the H
+  // items between them hide the AccH drain and the exchange.
+  auto n_own = [&](int bi) { return do_h ? (bi == 0 ? SH : SH - 2) : 0; };
+  auto n_next = [&](int bi) { return (do_h && bi + 1 < nb) ? 2 : 0; };
+  struct Gen { int bi, k, pos; };
+  auto item = [&](const Gen& gn, int& ty, int& blk, int& idx) {
+    const int o = n_own(gn.bi), x = n_next(gn.bi);
+    if (gn.k < o) { ty = 0; blk = gn.bi; idx = gn.bi == 0 ? gn.k : gn.k + 2; }
+    else if (gn.k < o + x) { ty = 0; blk = gn.bi + 1; idx = gn.k - o; }
+    else { ty = 1; blk = gn.bi; idx = gn.k - o - x; }
+  };
+  auto advance = [&](Gen& gn) {
+    ++gn.pos;
+    if (++gn.k == n_own(gn.bi) + n_next(gn.bi) + SW) { ++gn.bi; gn.k = 0; }
+  };
+  auto col0 = [&](int blk) { return (pi + blk * npairs) * BN; };
+  auto stage_of = [&](int blk, int j, uint32_t& ph) {
+    const int cnt = blk * SH + j;
+    ph = uint32_t(cnt / NSTAGE) & 1u;
+    return cnt % NSTAGE;
+  };
 
   // ---- setup: barriers, TMEM, constant operands ---------------------------
   if (threadIdx.x == 0) {
-    for (int s = 0; s < nstage; ++s) {
+    for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&bar_full[s], 1);
       mbar_init(&bar_empty[s], NEPI);
     }
-    for (int b = 0; b < 3; ++b) mbar_init(&bar_dfull[b], 1);
     for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar_dfull[b], 1);
       mbar_init(&bar_zfull[b], NEPI);
+      mbar_init(&bar_dempty[b], NEPI);
       mbar_init(&bar_zempty[b], 1);
     }
     mbar_init(bar_hp, NEPI);
     mbar_init(bar_hn, NEPI);
     mbar_init(bar_acch, 1);
+    mbar_init(bar_accfree, NEPI);
     mbar_init(bar_accw, 1);
-    mbar_init(bar_accw_free, NEPI);
+    mbar_init(bar_accwfree, NEPI);
     mbar_init(bar_wdone, 1);
+    mbar_init(bar_xfull, 1);
+    mbar_init(bar_xempty, NEPI);
     mbar_fence_init();
   }
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&mapH);
-    tma_prefetch(&mapW);
-  }
+  if (warp == 0 && lane == 0) tma_prefetch(&mapV);
   if (warp == 1) tmem_alloc<512>(s_tmem);
   if (warp >= 2) {
-    const int te = threadIdx.x - 64;
-    for (int i = te; i < L.FP * KP; i += NEPI * 32) {
-      const int f = i / KP, k = i - f * KP;
-      const bool ok = f < F && k < K;
-      const size_t gi = size_t(f) * K + k;
-      const uint32_t o = core_off(f, k), ot = coreT_off(k, f, L.FP);
+    // Wa (B of the H-side Vt product): [f x k] core tiles, hi then lo.
+    // chi1/chi2 (B of the H-side products): K-major over f, rows k (hi) and 16+k (lo).
+    for (int i = threadIdx.x - 64; i < FR * KP; i += NEPI * 32) {
+      const int fl = i / KP, k = i - fl * KP;
+      const bool ok = fl < FTr && k < K;
+      const size_t gi = size_t(row0 + fl) * K + k;
       float v, hi;
       v = ok ? Wa[gi] : 0.f; hi = tf32_hi(v);
-      sts_f32(s_base + L.off_wa + o, hi); sts_f32(s_base + L.off_wa + wb + o, v - hi);
+      sts_f32(sb + OFF_WA + core_off(fl, k), hi);
+      sts_f32(sb + OFF_WA + HILO + core_off(fl, k), v - hi);
       v = ok ? a.C1[gi] : 0.f; hi = tf32_hi(v);
-      sts_f32(s_base + L.off_c1 + ot, hi); sts_f32(s_base + L.off_c1 + wb + ot, v - hi);
+      sts_f32(sb + OFF_C1 + coreT_off(k, fl), hi);
+      sts_f32(sb + OFF_C1 + coreT_off(k + 16, fl), v - hi);
       v = ok ? a.C2[gi] : 0.f; hi = tf32_hi(v);
-      sts_f32(s_base + L.off_c2 + ot, hi); sts_f32(s_base + L.off_c2 + wb + ot, v - hi);
+      sts_f32(sb + OFF_C2 + coreT_off(k, fl), hi);
+      sts_f32(sb + OFF_C2 + coreT_off(k + 16, fl), v - hi);
     }
   }
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();   // peer barriers initialised before any remote op
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
-  // W~_p (A operand of the W-phase Vt MMAs) into TMEM: warps with g < FT write
-  // tile t = g, lane f, 16 hi + 16 lo columns.
-  if (warp >= 2) {
-    const int e = warp - 2, q = warp & 3, g = e >> 2;
-    if (g < L.FT) {
-      const int f = 128 * g + 32 * q + lane;
-      float hi[16], lo[16];
-#pragma unroll
-      for (int k = 0; k < KP; ++k) {
-        const float v = (f < F && k < K) ? Wt[size_t(f) * K + k] : 0.f;
-        hi[k] = tf32_hi(v);
-        lo[k] = v - hi[k];
-      }
-      const uint32_t ta = tmem + (uint32_t(32 * q) << 16) + TM_WT + 32 * g;
-      tmem_st16(ta, hi);
-      tmem_st16(ta + 16, lo);
-      tmem_st_wait();
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
 
   if (warp == 0) {
     // ======================= TMA producer ===================================
     if (lane == 0) {
-      int stage = 0;
-      uint32_t ph = 0;
-      for (int b = blockIdx.x; b < nblocks; b += gridDim.x) {
-        const int n0 = b * BN;
-        if (do_h) {
-          for (int j = 0; j < L.SH; ++j) {
-            mbar_wait(&bar_empty[stage], ph ^ 1);
-            mbar_expect_tx(&bar_full[stage], STAGE_BYTES);
-            tma_load_2d(smem + L.off_stage + stage * STAGE_BYTES, &mapH, &bar_full[stage], n0,
-                        32 * j);
-            if (++stage == nstage) { stage = 0; ph ^= 1; }
-          }
-        }
-        for (int w = 0; w < L.SW; ++w) {
-          mbar_wait(&bar_empty[stage], ph ^ 1);
-          mbar_expect_tx(&bar_full[stage], STAGE_BYTES);
-          tma_load_2d(smem + L.off_stage + stage * STAGE_BYTES, &mapW, &bar_full[stage],
-                      n0 + 32 * (w & 3), 128 * (w >> 2));
-          if (++stage == nstage) { stage = 0; ph ^= 1; }
+      for (int bi = 0; bi < nb; ++bi) {
+        const int n0 = col0(bi);
+        for (int j = 0; j < SH; ++j) {
+          uint32_t ph;
+          const int s = stage_of(bi, j, ph);
+          pwait(&bar_empty[s], ph ^ 1, 0);
+          mbar_expect_tx(&bar_full[s], STAGE_BYTES);
+          tma_load_2d(smem + OFF_STAGE + s * STAGE_BYTES, &mapV, &bar_full[s], n0, row0 + 32 * j);
         }
       }
     }
   } else if (warp == 1) {
     // ======================= MMA issuer (warp-uniform) ======================
-    // Sub-tiles are numbered c = bi * SB + s (s < SH: H phase, else W phase).
-    // D(c) is issued up to two sub-tiles ahead of the side MMAs of c, into
-    // one of three D buffers; the side MMAs of c wait for Z(c) from the
-    // epilogue and release the Z buffer through zempty.
-    const uint32_t id_big = idesc_tf32(128, 32, 0, 0);
-    const uint32_t id_side = idesc_tf32(128, 16, 0, 0);
-    const uint64_t d_wa = sdesc(s_base + L.off_wa, 128, 512);
-    const uint64_t d_hp = sdesc(s_base + L.off_hp, 128, 512);
-    const uint64_t d_hn = sdesc(s_base + L.off_hn, 128, 512);
-    const uint64_t d_c1 = sdesc(s_base + L.off_c1, 128, uint32_t(L.FP) * 32);
-    const uint64_t d_c2 = sdesc(s_base + L.off_c2, 128, uint32_t(L.FP) * 32);
-    const uint64_t d_hnt = sdesc(s_base + L.off_hnt, 128, BN * 32);
-    const int SHh = do_h ? L.SH : 0;
-    const int SB = SHh + L.SW;
-    const int nb_cta = blockIdx.x < nblocks ? (nblocks - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int total = a.debug >= 3 ? 0 : nb_cta * SB;
-    int nd = 0;
-    for (int cs = 0; cs < total; ++cs) {
-      // ---- issue D's ahead (three buffers) ----
-      while (nd < total && nd <= cs + 2) {
-        const int bi_d = nd / SB, s_d = nd - bi_d * SB;
-        const uint32_t dcol = tmem + TM_D + 32 * (nd % 3);
-        if (s_d < SHh) {
-          if (s_d == 0) {
-            mbar_wait(bar_hp, bi_d & 1);
-            tc_fence_after();
-          }
-          if (elect_one())
-            issue_big(dcol, d_hp, dplus(d_hp, hb), dplus(d_wa, s_d * 2048),
-                      dplus(d_wa, s_d * 2048 + wb), id_big, a.debug);
-        } else {
-          const int w = s_d - SHh, t = w >> 2, u = w & 3;
-          if (w == 0) {
-            // H~_p of this block needs every side MMA issued before it (the
-            // epilogue's H update waits for them): no run-ahead past here
-            if (cs < bi_d * SB + SHh) break;
-            mbar_wait(bar_hn, bi_d & 1);
-            tc_fence_after();
-          }
-          if (elect_one())
-            issue_big_ts(dcol, tmem + TM_WT + 32 * t, tmem + TM_WT + 32 * t + 16,
-                         dplus(d_hn, u * 2048), dplus(d_hn, u * 2048 + hb), id_big, a.debug);
+    // Two cursors over the item sequence: Vt tiles (D) run up to two items
+    // ahead of the side products.  D(x) reuses buffer x & 1 once the
+    // epilogue has loaded D(x-2) (dempty); side(x) waits for Z(x) (zfull)
+    // and releases its Z buffer through zempty.
+    const uint32_t id32 = idesc_tf32(128, 32, 0, 0);
+    const uint32_t id16 = idesc_tf32(128, 16, 0, 0);
+    const uint64_t d_wa = sdesc(sb + OFF_WA, 128, 512);
+    const uint64_t d_hn = sdesc(sb + OFF_HN, 128, 512);
+    const uint64_t d_c1 = sdesc(sb + OFF_C1, 128, 4096);
+    const uint64_t d_c2 = sdesc(sb + OFF_C2, 128, 4096);
+    const uint64_t d_hnt = sdesc(sb + OFF_HNT, 128, 4096);
+    Gen gd{0, 0, 0}, gs{0, 0, 0};
+    while (gs.bi < nb) {
+      const int ns = gs.pos;
+      // ---- Vt tiles up to two items ahead of the next side product ----
+      while (gd.bi < nb && gd.pos <= ns + 2) {
+        int ty, blk, idx;
+        item(gd, ty, blk, idx);
+        if (ty == 1 && idx == 0) {
+          // U2(blk) publishes H~_p after the side products up to last_dep
+          const int last_dep = gd.pos - 1 - n_next(blk);
+          if (last_dep >= ns) break;
         }
-        if (elect_one()) mma_commit(&bar_dfull[nd % 3]);
-        __syncwarp();
-        ++nd;
-      }
-      // ---- side MMAs of sub-tile cs ----
-      mbar_wait(&bar_zfull[cs & 1], (cs >> 1) & 1);
-      tc_fence_after();
-      const int bi = cs / SB, s_c = cs - bi * SB;
-      const uint32_t zb = tmem + TM_Z + 128 * (cs & 1);
-      if (s_c < SHh) {
-        const uint64_t b1 = dplus(d_c1, s_c * 1024);
-        const uint64_t b2 = dplus(d_c2, s_c * 1024);
+        if (gd.pos >= 2) {
+          pwait(&bar_dempty[gd.pos & 1], ((gd.pos - 2) >> 1) & 1, 0);
+        }
+        if (ty == 1 && idx == 0) {
+          BNMF_TRACE(6, gd.pos);
+          pwait(bar_hn, blk & 1, 1);
+          BNMF_TRACE(7, gd.pos);
+        } else if (ty == 0 && idx == 0) {
+          pwait(bar_hp, blk & 1, 2);
+        }
+        tc_fence_after();
+        const uint32_t dcol = tmem + TM_D + 32 * (gd.pos & 1);
+        BNMF_PROF_T0(tdi);
+        BNMF_TRACE(1, gd.pos);
         if (elect_one()) {
-          issue_side(tmem + TM_ACCH, zb, zb + 32, b1, dplus(b1, wb), id_side, s_c == 0, a.debug);
-          if (!den_ones)
-            issue_side(tmem + TM_ACCH + 16, zb + 64, zb + 96, b2, dplus(b2, wb), id_side, s_c == 0,
-                       a.debug);
-          mma_commit(&bar_zempty[cs & 1]);
-          if (s_c == SHh - 1) mma_commit(bar_acch);
+          if (ty == 0)
+            issue_vt(dcol, tmem + TM_HP, tmem + TM_HP + 16, dplus(d_wa, idx * 2048),
+                     dplus(d_wa, idx * 2048 + HILO), id32);
+          else
+            issue_vt(dcol, tmem + TM_WT, tmem + TM_WT + 16, dplus(d_hn, idx * 2048),
+                     dplus(d_hn, idx * 2048 + HILO), id32);
+          mma_commit(&bar_dfull[gd.pos & 1]);
         }
         __syncwarp();
-      } else {
-        const int w = s_c - SHh, t = w >> 2, u = w & 3;
-        const bool fresh = (bi % FOLD) == 0 && u == 0;
-        if (w == 0 && (bi % FOLD) == 0 && bi > 0) {
-          mbar_wait(bar_accw_free, ((bi / FOLD) - 1) & 1);
+        BNMF_PROF_ADD(6, tdi);
+        BNMF_TRACE(2, gd.pos);
+        advance(gd);
+      }
+      // ---- side products of item ns ----
+      int ty, blk, idx;
+      item(gs, ty, blk, idx);
+      BNMF_TRACE(3, ns);
+      pwait(&bar_zfull[ns & 1], (ns >> 1) & 1, 3);
+      BNMF_TRACE(4, ns);
+      tc_fence_after();
+      const uint32_t zb = tmem + TM_Z + 128 * (ns & 1);
+      BNMF_PROF_T0(tsi);
+      if (ty == 0) {
+        if (idx == 0 && blk > 0) {
+          pwait(bar_accfree, (blk - 1) & 1, 4);
           tc_fence_after();
         }
-        const uint64_t bh = dplus(d_hnt, u * 1024);
-        const uint64_t bl = dplus(bh, hb);
-        const bool last_w = w == L.SW - 1;
-        const bool fold_end = (bi % FOLD) == FOLD - 1 || bi == nb_cta - 1;
         if (elect_one()) {
-          issue_side(tmem + TM_ACCW + 32 * t, zb, zb + 32, bh, bl, id_side, fresh, a.debug);
-          issue_side(tmem + TM_ACCW + 32 * t + 16, zb + 64, zb + 96, bh, bl, id_side, fresh, a.debug);
-          mma_commit(&bar_zempty[cs & 1]);
-          if (last_w && fold_end) mma_commit(bar_accw);
-          if (last_w) mma_commit(bar_wdone);
+          issue_side(tmem + TM_ACCH, zb, dplus(d_c1, idx * 1024), id32, id16, idx == 0);
+          if (!den_ones)
+            issue_side(tmem + TM_ACCH + 32, zb + 16, dplus(d_c2, idx * 1024), id32, id16, idx == 0);
+          mma_commit(&bar_zempty[ns & 1]);
+          if (idx == SH - 1) mma_commit(bar_acch);
         }
-        __syncwarp();
+      } else {
+        const bool fresh = (blk % FOLD) == 0 && idx == 0;
+        if (fresh && blk > 0) {
+          pwait(bar_accwfree, ((blk / FOLD) - 1) & 1, 5);
+          tc_fence_after();
+        }
+        const bool fold_end = (blk % FOLD) == FOLD - 1 || blk == nb - 1;
+        if (elect_one()) {
+          const uint64_t bh = dplus(d_hnt, idx * 1024);
+          issue_side(tmem + TM_ACCW, zb, bh, id32, id16, fresh);
+          issue_side(tmem + TM_ACCW + 32, zb + 16, bh, id32, id16, fresh);
+          mma_commit(&bar_zempty[ns & 1]);
+          if (idx == SW - 1) {
+            mma_commit(bar_wdone);
+            if (fold_end) mma_commit(bar_accw);
+          }
+        }
       }
+      __syncwarp();
+      BNMF_PROF_ADD(7, tsi);
+      BNMF_TRACE(5, ns);
+      advance(gs);
     }
-    __syncwarp();
   } else {
     // ======================= epilogue =======================================
     const int e = warp - 2;
     const int q = warp & 3;          // TMEM lane quadrant
-    const int g = e >> 2;            // 8-column slice of a 32-wide sub-tile
-    const int row = 32 * q + lane;   // TMEM lane (n in the H phase, f_local in the W phase)
+    const int g = e >> 2;            // 8-column slice of an item / 4-wide k group
+    const int row = 32 * q + lane;   // TMEM lane: n (H items, U) or f - row0 (W items)
     const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16);
     double obj = 0.0;
-    float hprev[4];
-    int stage = 0;
-    uint32_t ph = 0;
-    uint32_t c = 0;
-    int bi = 0;
     int nfold = 0;
     double* mypart = a.part + size_t(blockIdx.x) * 2 * F * K;
-
-    // H~_{p-1} rows of a block (this thread: n = row, k in [4g, 4g+4))
-    auto load_hprev = [&](int n0) {
-      const int n = n0 + row;
+    // H-update constants in fp32 (FP64 throughput is low on this part; the
+    // update ratio is formed and stored in fp32 anyway)
+    float nrm[4], cs2[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = 4 * g + i;
+      nrm[i] = (do_h && k < K) ? float(a.norms[k]) : 0.f;
+      cs2[i] = (do_h && den_ones && k < K) ? float(a.csum2[k]) : 1.f;
+    }
+    const float gam = float(a.sc.gamma);
+    const float floor_f = fmaxf(float(a.sc.floor), 1.17549435e-38f);
+    // H~_{p-1} rows of blocks u, u+1, u+2 (u = next block to finish its H update)
+    float h0[4], h1[4], h2[4];
+    int ucur = 0;
+    auto load_rows = [&](int blk, float* h) {
+      const int n = col0(blk) + row;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int k = 4 * g + i;
-        hprev[i] = (n < N && k < K) ? Hprev[size_t(n) * K + k] : 0.f;
-        const float hi = tf32_hi(hprev[i]);
-        const uint32_t o = s_base + L.off_hp + core_off(row, k);
-        sts_f32(o, hi);
-        sts_f32(o + hb, hprev[i] - hi);
+        h[i] = (blk < nb && n < N && k < K) ? Hprev[size_t(n) * K + k] : 0.f;
       }
     };
-    auto store_hnew = [&](int n0, const float* hv) {
-      const int n = n0 + row;
+    // H~_{p-1} rows of a block as the TMEM A operand of the H-side Vt tiles
+    auto write_hp = [&](const float* h) {
+      float hi[4], lo[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int k = 4 * g + i;
-        const float v = (n < N && k < K) ? hv[i] : 0.f;
-        if (do_h && n < N && k < K) Hnew[size_t(n) * K + k] = v;
-        const float hi = tf32_hi(v);
-        const uint32_t o = s_base + L.off_hn + core_off(row, k);
-        const uint32_t ot = s_base + L.off_hnt + coreT_off(k, row, BN);
-        sts_f32(o, hi);
-        sts_f32(o + hb, v - hi);
-        sts_f32(ot, hi);
-        sts_f32(ot + hb, v - hi);
-      }
-    };
-    // add the TMEM W sums of the last FOLD blocks into the fp64 slab
-    auto fold = [&]() {
-      if (a.debug >= 3) { ++nfold; return; }
-      mbar_wait(bar_accw, nfold & 1);
-      tc_fence_after();
-      if (g < 2 * L.FT) {
-        const int t = g >> 1, s = g & 1;   // tile, num/den
-        float v[16];
-        tmem_ld16(lane_base + TM_ACCW + 32 * t + 16 * s, v);
-        const int f = 128 * t + row;
-        if (f < F) {
-          double* dst = mypart + size_t(s) * F * K + size_t(f) * K;
-#pragma unroll
-          for (int k = 0; k < KP; ++k)
-            if (k < K) dst[k] = (nfold == 0 ? 0.0 : dst[k]) + double(v[k]);
-        }
-      }
+      for (int i = 0; i < 4; ++i) { hi[i] = tf32_hi(h[i]); lo[i] = h[i] - hi[i]; }
+      tmem_st4(lane_base + TM_HP + 4 * g, hi);
+      tmem_st4(lane_base + TM_HP + 16 + 4 * g, lo);
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar_accw_free);
-      ++nfold;
+      if (lane == 0) mbar_arrive(bar_hp);
     };
 
-    int b = blockIdx.x;
-    if (b < nblocks) {
-      load_hprev(b * BN);
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_hp);
+    // W~_p rows of this CTA into TMEM (A operand of the W-side Vt tiles)
+    {
+      float hi[4], lo[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int k = 4 * g + i;
+        const float v = (row < FTr && k < K) ? Wt[size_t(row0 + row) * K + k] : 0.f;
+        hi[i] = tf32_hi(v);
+        lo[i] = v - hi[i];
+      }
+      tmem_st4(lane_base + TM_WT + 4 * g, hi);
+      tmem_st4(lane_base + TM_WT + 16 + 4 * g, lo);
+      tmem_st_wait();
     }
-    for (; b < nblocks; b += gridDim.x, ++bi) {
-      const int n0 = b * BN;
-      const bool ncols_full = n0 + BN <= N;
+    load_rows(0, h0);
+    load_rows(1, h1);
+    load_rows(2, h2);
+    if (do_h && nb > 0) write_hp(h0);
+    else tc_fence_before();
+
+    // U1(blk): AccH of the block read out (and sent to the peer CTA)
+    float unum[4], uden[4];
+    auto do_u1 = [&](int blk) {
+      pwait(bar_acch, blk & 1, 3);
+      BNMF_TRACE(48, blk);
+      tc_fence_after();
+      uint32_t r[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%16];\n\t"
+          "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4,%5,%6,%7}, [%17];\n\t"
+          "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%8,%9,%10,%11}, [%18];\n\t"
+          "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%12,%13,%14,%15}, [%19];\n\t"
+          "tcgen05.wait::ld.sync.aligned;"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+            "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          : "r"(lane_base + TM_ACCH + 4 * g), "r"(lane_base + TM_ACCH + 16 + 4 * g),
+            "r"(lane_base + TM_ACCH + 32 + 4 * g), "r"(lane_base + TM_ACCH + 48 + 4 * g)
+          : "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_accfree);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        unum[i] = __uint_as_float(r[i]) + __uint_as_float(r[4 + i]);
+        uden[i] = den_ones ? 0.f : __uint_as_float(r[8 + i]) + __uint_as_float(r[12 + i]);
+      }
+      if (CL > 1) {
+        const uint32_t peer = rank ^ 1u;
+        if (blk > 0) pwait_cl(bar_xempty, (blk - 1) & 1, 4);
+        if (threadIdx.x == 64) mbar_expect_tx_u32(smem_u32(bar_xfull), BN * 2 * KP * 4);
+        const uint32_t my0 = sb + OFF_XCH + uint32_t(((2 * g) * BN + row) * 16);
+        const uint32_t rbar = mapa_shared(smem_u32(bar_xfull), peer);
+        st_async_v4(mapa_shared(my0, peer), make_float4(unum[0], unum[1], unum[2], unum[3]), rbar);
+        st_async_v4(mapa_shared(my0 + BN * 16, peer), make_float4(uden[0], uden[1], uden[2], uden[3]),
+                    rbar);
+      }
+    };
+    // U2(blk): peer partial added (fp32 a + b is commutative, so both CTAs
+    // form bitwise-identical totals), H~_p = H~_{p-1} (num/den)^gamma norms
+    // published to SMEM (and HBM)
+    auto do_u2 = [&](int blk) {
+      const int n = col0(blk) + row;
+      float hv[4];
       if (do_h) {
-        // ---------------- H phase ----------------
-        for (int j = 0; j < L.SH; ++j, ++c) {
-          const uint32_t buf = c & 1, dbuf = c % 3;
-          const bool nomma = a.debug >= 3;
-          if (!nomma) mbar_wait(&bar_dfull[dbuf], (c / 3) & 1);
-          mbar_wait(&bar_full[stage], ph);
-          tc_fence_after();
-          float y[8], x[8], zn[8], zd[8];
-          if (!nomma) tmem_ld8(lane_base + TM_D + 32 * dbuf + 8 * g, y);
-          else for (int i = 0; i < 8; ++i) y[i] = 1.f;
-          const uint32_t xa = s_base + L.off_stage + stage * STAGE_BYTES + (8 * g * 128 + row) * 4;
-          if (a.debug == 1 || a.debug == 4) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) { zn[i] = y[i]; zd[i] = y[i]; }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) x[i] = lds_f32(xa + i * 512);
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              zpair<FBC>(x[i], KAPPA ? y[i] + kappa : y[i], beta, zn[i], zd[i]);
-          }
-          if (!(ncols_full && 32 * j + 32 <= F)) {
-            const bool nok = n0 + row < N;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const bool ok = nok && (32 * j + 8 * g + i < F);
-              zn[i] = ok ? zn[i] : 0.f;
-              zd[i] = ok ? zd[i] : 0.f;
-            }
-          }
-          const uint32_t zb = lane_base + TM_Z + 128 * buf + 8 * g;
-          if (c >= 2 && !nomma) {   // side MMAs of c-2 released this Z buffer
-            mbar_wait(&bar_zempty[buf], ((c - 2) >> 1) & 1);
-            tc_fence_after();
-          }
-          if (!nomma) {
-            store_z8(zb, zn);
-            if (!den_ones) store_z8(zb + 64, zd);
-          } else if (zn[0] == 12345.f && zd[1] == 1.f) {
-            obj += 1.0;
-          }
-          tmem_st_wait();
-          tc_fence_before();
+        if (CL > 1) {
+          const uint32_t peer = rank ^ 1u;
+          const uint32_t my0 = sb + OFF_XCH + uint32_t(((2 * g) * BN + row) * 16);
+          pwait_cl(bar_xfull, blk & 1, 5);
+          BNMF_TRACE(43, blk);
+          const float4 pn = lds_f128(my0), pd = lds_f128(my0 + BN * 16);
+          unum[0] += pn.x; unum[1] += pn.y; unum[2] += pn.z; unum[3] += pn.w;
+          uden[0] += pd.x; uden[1] += pd.y; uden[2] += pd.z; uden[3] += pd.w;
+          BNMF_TRACE(49, blk);
           __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(&bar_zfull[buf]);
-            mbar_arrive(&bar_empty[stage]);
-          }
-          if (++stage == nstage) { stage = 0; ph ^= 1; }
-        }
-        // ---------------- H update ----------------
-        float nv[4], dv[4], hv[4];
-        if (a.debug < 3) {
-          mbar_wait(bar_acch, bi & 1);
-          tc_fence_after();
-          tmem_ld4(lane_base + TM_ACCH + 4 * g, nv);
-          if (!den_ones) tmem_ld4(lane_base + TM_ACCH + 16 + 4 * g, dv);
-        } else {
-          for (int i = 0; i < 4; ++i) { nv[i] = 1.f; dv[i] = 1.f; }
+          if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(bar_xempty), peer));
+          BNMF_TRACE(50, blk);
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int k = 4 * g + i;
           float v = 0.f;
           if (k < K) {
-            const double den = den_ones ? a.csum2[k] : double(dv[i]);
-            const double r = double(nv[i]) / fmax(den, a.sc.floor);
-            v = float(double(hprev[i]) * apply_exponent<double>(r, a.sc.gamma) * a.norms[k]);
+            const float dn = den_ones ? cs2[i] : uden[i];
+            const float r = __fdiv_rn(unum[i], fmaxf(dn, floor_f));
+            const float rg = gam == 1.f ? r : (gam == 0.5f ? sqrtf(r) : powf(r, gam));
+            v = h0[i] * rg * nrm[i];
           }
           hv[i] = v;
         }
-        tc_fence_before();
-        if (bi > 0 && a.debug < 3) mbar_wait(bar_wdone, (bi - 1) & 1);   // W MMAs of bi-1 read H~ smem
-        store_hnew(n0, hv);
       } else {
-        if (bi > 0 && a.debug < 3) mbar_wait(bar_wdone, (bi - 1) & 1);
-        store_hnew(n0, hprev);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) hv[i] = n < N ? h0[i] : 0.f;
+      }
+      BNMF_TRACE(45, blk);
+      if (blk > 0) pwait(bar_wdone, (blk - 1) & 1, 6);   // W MMAs of blk-1 read Hn/HnT
+      BNMF_TRACE(46, blk);
+      {
+        // Hn: this thread's 4 k of row n are one 16 B chunk of the core tile
+        float hi[4], lo[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { hi[i] = tf32_hi(hv[i]); lo[i] = hv[i] - hi[i]; }
+        sts_f128(sb + OFF_HN + core_off(row, 4 * g), hi[0], hi[1], hi[2], hi[3]);
+        sts_f128(sb + OFF_HN + HILO + core_off(row, 4 * g), lo[0], lo[1], lo[2], lo[3]);
+        // HnT (K-major over n): transpose 4 x 4 within lane quads so that
+        // lane 4m + j holds k = 4g + j of rows 4m .. 4m + 3 (one 16 B chunk)
+        const int j = lane & 3;
+        float tv[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int si = (j - r) & 3;   // this lane sends its value for k index si
+          const float send = si == 0 ? hv[0] : si == 1 ? hv[1] : si == 2 ? hv[2] : hv[3];
+          const float got = __shfl_sync(0xffffffffu, send, (lane & ~3) | ((j + r) & 3));
+          const int dr = (j + r) & 3;   // received: row 4m + dr, k index j
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (t == dr) tv[t] = got;
+        }
+        float th[4], tl[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) { th[t] = tf32_hi(tv[t]); tl[t] = tv[t] - th[t]; }
+        const int rb = row & ~3;
+        sts_f128(sb + OFF_HNT + coreT_off(4 * g + j, rb), th[0], th[1], th[2], th[3]);
+        sts_f128(sb + OFF_HNT + coreT_off(4 * g + j + 16, rb), tl[0], tl[1], tl[2], tl[3]);
       }
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_hn);
-      // prefetch the next block's H~_{p-1} rows (D1 MMAs of this block are done)
-      if (b + (int)gridDim.x < nblocks) {
-        load_hprev((b + gridDim.x) * BN);
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_hp);
+      BNMF_TRACE(47, blk);
+      // global traffic only after the SMEM publish (the proxy fence above
+      // would otherwise wait for these stores)
+      if (do_h && (CL == 1 || (g >> 1) == int(rank)) && n < N) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (4 * g + i < K) Hnew[size_t(n) * K + 4 * g + i] = hv[i];
       }
-      // ---------------- W phase ----------------
-      for (int w = 0; w < L.SW; ++w, ++c) {
-        const uint32_t buf = c & 1, dbuf = c % 3;
-        const int t = w >> 2, u = w & 3;
-        const bool nomma = a.debug >= 3;
-        if (!nomma) mbar_wait(&bar_dfull[dbuf], (c / 3) & 1);
-        mbar_wait(&bar_full[stage], ph);
-        tc_fence_after();
-        float y[8], x[8], zn[8], zd[8], dd[8];
-        if (!nomma) tmem_ld8(lane_base + TM_D + 32 * dbuf + 8 * g, y);
-        else for (int i = 0; i < 8; ++i) y[i] = 1.f;
-        const uint32_t ta = s_base + L.off_stage + stage * STAGE_BYTES + row * 128;
-        if (a.debug == 1 || a.debug == 4) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) { zn[i] = y[i]; zd[i] = y[i]; dd[i] = 0.f; }
-        } else {
+      for (int i = 0; i < 4; ++i) { h0[i] = h1[i]; h1[i] = h2[i]; }
+      load_rows(blk + 3, h2);
+      ucur = blk + 1;
+    };
+
+    // add the TMEM W sums of the last FOLD blocks into the fp64 slab
+    auto fold = [&]() {
+      pwait(bar_accw, nfold & 1, 7);
+      tc_fence_after();
+      const int s = g >> 1, h = g & 1;   // num/den, k half
+      float v0[8], v1[8];
+      tmem_ld8(lane_base + TM_ACCW + 32 * s + 8 * h, v0);
+      tmem_ld8(lane_base + TM_ACCW + 32 * s + 16 + 8 * h, v1);
+      if (row < FTr) {
+        double* dst = mypart + size_t(s) * F * K + size_t(row0 + row) * K;
 #pragma unroll
-          for (int cq = 0; cq < 2; ++cq) {
-            const float4 v4 = lds_f128(ta + (((2 * g + cq) ^ (row & 7)) << 4));
-            x[4 * cq + 0] = v4.x; x[4 * cq + 1] = v4.y; x[4 * cq + 2] = v4.z; x[4 * cq + 3] = v4.w;
-          }
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float yy = KAPPA ? y[i] + kappa : y[i];
-            zpair<FBC>(x[i], yy, beta, zn[i], zd[i]);
-            dd[i] = dterm<FBC>(x[i], yy, zd[i], beta);
-          }
-        }
-        if (!(ncols_full && 128 * t + 128 <= F)) {
-          const int f = 128 * t + row;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const bool ok = f < F && (n0 + 32 * u + 8 * g + i < N);
-            zn[i] = ok ? zn[i] : 0.f;
-            zd[i] = ok ? zd[i] : 0.f;
-            dd[i] = ok ? dd[i] : 0.f;
+        for (int kk = 0; kk < 8; ++kk) {
+          const int k = 8 * h + kk;
+          // one owner thread per slab element: the first fold stores, later
+          // folds are fire-and-forget fp64 reductions applied in program order
+          if (k < K) {
+            const double add = double(v0[kk]) + double(v1[kk]);
+            if (nfold == 0) dst[k] = add;
+            else atomicAdd(dst + k, add);
           }
         }
-        obj += double((dd[0] + dd[1]) + (dd[2] + dd[3]) + ((dd[4] + dd[5]) + (dd[6] + dd[7])));
-        const uint32_t zb = lane_base + TM_Z + 128 * buf + 8 * g;
-        if (c >= 2 && !nomma) {
-          mbar_wait(&bar_zempty[buf], ((c - 2) >> 1) & 1);
-          tc_fence_after();
-        }
-        if (!nomma) {
-          store_z8(zb, zn);
-          store_z8(zb + 64, zd);
-        } else if (zn[0] == 12345.f && zd[1] == 1.f) {
-          obj += 1.0;
-        }
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&bar_zfull[buf]);
-          mbar_arrive(&bar_empty[stage]);
-        }
-        if (++stage == nstage) { stage = 0; ph ^= 1; }
       }
-      if ((bi % FOLD) == FOLD - 1 || b + (int)gridDim.x >= nblocks) fold();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_accwfree);
+      ++nfold;
+    };
+
+    const bool rows_full = FTr == 32 * SH;
+    int c = 0;   // item counter (Vt / Z buffer c & 1)
+    float objb = 0.f;   // objective of the current block (fp32, 32 terms per thread)
+    // Vt tile of item c -> registers; the buffer is handed back right away
+    auto load_d = [&](int buf, float* y) {
+      tmem_ld8(lane_base + TM_D + 32 * buf + 8 * g, y);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_dempty[buf]);
+    };
+    // Z of item c -> TMEM (after the side products of item c - 2 retired)
+    auto put_z = [&](int buf, const float* zn, const float* zd) {
+      if (c >= 2) pwait(&bar_zempty[buf], ((c - 2) >> 1) & 1, 6);
+      tc_fence_after();
+      store_z(lane_base + TM_Z + 128 * buf + 32 * g, zn, zd);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_zfull[buf]);
+      BNMF_TRACE(22, c);
+      ++c;
+    };
+    // ---------------- H item: rows row0 + 32 idx + [0, 32) of block blk ----------------
+    auto h_item = [&](int blk, int idx) {
+      const int buf = c & 1;
+      const int n0 = col0(blk);
+      uint32_t ph;
+      const int s = stage_of(blk, idx, ph);
+      BNMF_TRACE(20, c);
+      pwait(&bar_dfull[buf], (c >> 1) & 1, 0);
+      BNMF_TRACE(21, c);
+      pwait(&bar_full[s], ph, 1);
+      tc_fence_after();
+      float y[8], zn[8], zd[8];
+      load_d(buf, y);
+      if (idx == SH - 1 && blk + 1 < nb) {   // Vt tiles of blk are done: stage H~ of blk + 1
+        const bool first = blk + 1 == ucur + 1;
+        float t[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) t[i] = first ? h1[i] : h2[i];
+        write_hp(t);
+      }
+      const uint32_t xa = sb + OFF_STAGE + s * STAGE_BYTES + (8 * g) * VROWB + row * 4;
+      float x[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = lds_f32(xa + i * VROWB);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) zpair<FBC>(x[i], KAPPA ? y[i] + kappa : y[i], beta, zn[i], zd[i]);
+      if (!(n0 + BN <= N && (rows_full || 32 * idx + 32 <= FTr))) {
+        const bool nok = n0 + row < N;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const bool ok = nok && (32 * idx + 8 * g + i < FTr);
+          zn[i] = ok ? zn[i] : 0.f;
+          zd[i] = ok ? zd[i] : 0.f;
+        }
+      }
+      put_z(buf, zn, zd);
+    };
+    // ---------------- W item: columns n0 + 32 idx + [0, 32) of block blk ----------------
+    auto w_item = [&](int blk, int idx, uint32_t xrow) {
+      const int buf = c & 1;
+      const int n0 = col0(blk);
+      BNMF_TRACE(30, c);
+      pwait(&bar_dfull[buf], (c >> 1) & 1, 2);
+      BNMF_TRACE(31, c);
+      tc_fence_after();
+      float y[8], x[8], zn[8], zd[8], dd[8];
+      load_d(buf, y);
+      if (q < SH) {
+        const uint32_t xa = xrow + (32 * idx + 8 * g) * 4;
+        const float4 v0 = lds_f128(xa), v1 = lds_f128(xa + 16);
+        x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
+        x[4] = v1.x; x[5] = v1.y; x[6] = v1.z; x[7] = v1.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float yy = KAPPA ? y[i] + kappa : y[i];
+        zpair<FBC>(x[i], yy, beta, zn[i], zd[i]);
+        dd[i] = dterm<FBC>(x[i], yy, zd[i], beta);
+      }
+      if (!(n0 + BN <= N && row < FTr)) {
+        const bool fok = row < FTr;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const bool ok = fok && (n0 + 32 * idx + 8 * g + i < N);
+          zn[i] = ok ? zn[i] : 0.f;
+          zd[i] = ok ? zd[i] : 0.f;
+          dd[i] = ok ? dd[i] : 0.f;
+        }
+      }
+      objb += (dd[0] + dd[1]) + (dd[2] + dd[3]) + ((dd[4] + dd[5]) + (dd[6] + dd[7]));
+      put_z(buf, zn, zd);
+    };
+
+    for (int bi = 0; bi < nb; ++bi) {
+      if (do_h) {
+        for (int j = bi == 0 ? 0 : 2; j < SH; ++j) h_item(bi, j);
+      } else {
+        for (int j = 0; j < SH; ++j) {
+          uint32_t ph;
+          const int s = stage_of(bi, j, ph);
+          mbar_wait(&bar_full[s], ph);
+        }
+      }
+      {
+        if (do_h) {
+          if (bi + 1 < nb) h_item(bi + 1, 0);
+          BNMF_PROF_T0(tu1);
+          BNMF_TRACE(40, c);
+          do_u1(bi);
+          BNMF_TRACE(41, c);
+          BNMF_PROF_ADD(8, tu1);
+          if (bi + 1 < nb) h_item(bi + 1, 1);
+        }
+        BNMF_PROF_T0(tu2);
+        BNMF_TRACE(42, c);
+        do_u2(bi);
+        BNMF_TRACE(44, c);
+        BNMF_PROF_ADD(9, tu2);
+      }
+      uint32_t phq;
+      const uint32_t xrow = sb + OFF_STAGE + stage_of(bi, q < SH ? q : 0, phq) * STAGE_BYTES + lane * VROWB;
+      objb = 0.f;
+      for (int u = 0; u < SW; ++u) w_item(bi, u, xrow);
+      obj += double(objb);
+      if (lane == 0)
+        for (int j = 0; j < SH; ++j) {
+          uint32_t ph;
+          mbar_arrive(&bar_empty[stage_of(bi, j, ph)]);
+        }
+      if ((bi % FOLD) == FOLD - 1 || bi == nb - 1) {
+        BNMF_PROF_T0(tf);
+        BNMF_TRACE(50, c);
+        fold();
+        BNMF_TRACE(51, c);
+        BNMF_PROF_ADD(10, tf);
+      }
     }
-    if (nfold == 0 && g < 2 * L.FT) {   // CTA without blocks: zero slab rows
-      const int t = g >> 1, s = g & 1;
-      const int f = 128 * t + row;
-      if (f < F)
-        for (int k = 0; k < K; ++k) mypart[size_t(s) * F * K + size_t(f) * K + k] = 0.0;
+    if (nfold == 0) {   // CTA without blocks: zero its slab rows
+      const int s = g >> 1, h = g & 1;
+      if (row < FTr)
+        for (int kk = 0; kk < 8; ++kk) {
+          const int k = 8 * h + kk;
+          if (k < K) mypart[size_t(s) * F * K + size_t(row0 + row) * K + k] = 0.0;
+        }
     }
     for (int o = 16; o > 0; o >>= 1) obj += __shfl_down_sync(0xffffffffu, obj, o);
     if (lane == 0) s_red[e] = obj;
   }
+#ifdef BNMF_TC_PROF
+  if (trace_buf) trace_buf[4095] = trace_n;
+  if (rec) pcs[pbase + 11] = clock64() - t_start;
+  __syncthreads();
+  if (prof)
+    for (int i = threadIdx.x; i < 48; i += blockDim.x) prof[i] = (long long)pcs[i];
+#endif
+#undef BNMF_PROF_T0
+#undef BNMF_PROF_ADD
+#undef BNMF_TRACE
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -643,6 +816,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapH,
     for (int i = 0; i < NEPI; ++i) t += s_red[i];
     a.opart[blockIdx.x] = t;
   }
+  if (CL > 1) cluster_sync_all();   // no CTA leaves while its peer may still signal it
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 

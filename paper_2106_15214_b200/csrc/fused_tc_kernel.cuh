@@ -173,8 +173,6 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
   uint64_t* bar_empty = bars + 8;     // [NSTAGE] epilogue -> TMA
   uint64_t* bar_dfull = bars + 16;    // [2] Vt tile ready
   uint64_t* bar_zfull = bars + 18;    // [2] Z written
-  uint64_t* bar_dempty = bars + 32;   // [2] Vt tile loaded by the epilogue
-  uint64_t* bar_zempty = bars + 34;   // [2] side products of a Z buffer retired
   uint64_t* bar_hp = bars + 22;       // H~_{p-1} of the next block in TMEM
   uint64_t* bar_hn = bars + 23;       // H~_p of the block in SMEM
   uint64_t* bar_acch = bars + 24;     // AccH of the block complete
@@ -243,24 +241,12 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
   const int den_ones = a.den_ones;
   const float kappa = float(a.sc.kappa), beta = float(a.sc.beta);
 
-  // item sequence of this CTA (identical in the MMA warp and the epilogue):
-  // block bi lists its own H items (all of them for bi == 0, else 2..SH-1),
-  // then H(bi+1, 0) [U1(bi)] H(bi+1, 1) [U2(bi)], then W(bi, 0..SW-1).  U1
-  // reads AccH and sends it to the peer, U2 finishes the H update; the H
-  // items between them hide the AccH drain and the exchange.
-  auto n_own = [&](int bi) { return do_h ? (bi == 0 ? SH : SH - 2) : 0; };
-  auto n_next = [&](int bi) { return (do_h && bi + 1 < nb) ? 2 : 0; };
-  struct Gen { int bi, k, pos; };
-  auto item = [&](const Gen& gn, int& ty, int& blk, int& idx) {
-    const int o = n_own(gn.bi), x = n_next(gn.bi);
-    if (gn.k < o) { ty = 0; blk = gn.bi; idx = gn.bi == 0 ? gn.k : gn.k + 2; }
-    else if (gn.k < o + x) { ty = 0; blk = gn.bi + 1; idx = gn.k - o; }
-    else { ty = 1; blk = gn.bi; idx = gn.k - o - x; }
-  };
-  auto advance = [&](Gen& gn) {
-    ++gn.pos;
-    if (++gn.k == n_own(gn.bi) + n_next(gn.bi) + SW) { ++gn.bi; gn.k = 0; }
-  };
+  // item sequence of this CTA (the MMA warp and the epilogue walk it in the
+  // same order): block bi lists its own H items (all of them for bi == 0,
+  // else 2..SH-1), then H(bi+1, 0) [U1(bi)] H(bi+1, 1) [U2(bi)], then
+  // W(bi, 0..SW-1).  U1 reads AccH and sends it to the peer CTA, U2 finishes
+  // the H update; the H items between them hide the AccH drain and the
+  // exchange.
   auto col0 = [&](int blk) { return (pi + blk * npairs) * BN; };
   auto stage_of = [&](int blk, int j, uint32_t& ph) {
     const int cnt = blk * SH + j;
@@ -277,8 +263,6 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bar_dfull[b], 1);
       mbar_init(&bar_zfull[b], NEPI);
-      mbar_init(&bar_dempty[b], NEPI);
-      mbar_init(&bar_zempty[b], 1);
     }
     mbar_init(bar_hp, NEPI);
     mbar_init(bar_hn, NEPI);
@@ -335,10 +319,10 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
     }
   } else if (warp == 1) {
     // ======================= MMA issuer (warp-uniform) ======================
-    // Two cursors over the item sequence: Vt tiles (D) run up to two items
-    // ahead of the side products.  D(x) reuses buffer x & 1 once the
-    // epilogue has loaded D(x-2) (dempty); side(x) waits for Z(x) (zfull)
-    // and releases its Z buffer through zempty.
+    // Straight-line per block, Vt tile of the next item issued before the
+    // side products of the current one: D(c) follows side(c-2), so its commit
+    // (dfull) also tells the epilogue that Z buffer c & 1 is free, and
+    // zfull(c - 2) (waited before side(c - 2)) told us Vt buffer c & 1 was read.
     const uint32_t id32 = idesc_tf32(128, 32, 0, 0);
     const uint32_t id16 = idesc_tf32(128, 16, 0, 0);
     const uint64_t d_wa = sdesc(sb + OFF_WA, 128, 512);
@@ -346,89 +330,119 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
     const uint64_t d_c1 = sdesc(sb + OFF_C1, 128, 4096);
     const uint64_t d_c2 = sdesc(sb + OFF_C2, 128, 4096);
     const uint64_t d_hnt = sdesc(sb + OFF_HNT, 128, 4096);
-    Gen gd{0, 0, 0}, gs{0, 0, 0};
-    while (gs.bi < nb) {
-      const int ns = gs.pos;
-      // ---- Vt tiles up to two items ahead of the next side product ----
-      while (gd.bi < nb && gd.pos <= ns + 2) {
-        int ty, blk, idx;
-        item(gd, ty, blk, idx);
-        if (ty == 1 && idx == 0) {
-          // U2(blk) publishes H~_p after the side products up to last_dep
-          const int last_dep = gd.pos - 1 - n_next(blk);
-          if (last_dep >= ns) break;
-        }
-        if (gd.pos >= 2) {
-          pwait(&bar_dempty[gd.pos & 1], ((gd.pos - 2) >> 1) & 1, 0);
-        }
-        if (ty == 1 && idx == 0) {
-          BNMF_TRACE(6, gd.pos);
-          pwait(bar_hn, blk & 1, 1);
-          BNMF_TRACE(7, gd.pos);
-        } else if (ty == 0 && idx == 0) {
-          pwait(bar_hp, blk & 1, 2);
-        }
+    int nd = 0, ns = 0, w0_issued = -1;
+    auto d_h = [&](int blk, int j) {
+      if (j == 0) {
+        pwait(bar_hp, blk & 1, 2);
         tc_fence_after();
-        const uint32_t dcol = tmem + TM_D + 32 * (gd.pos & 1);
-        BNMF_PROF_T0(tdi);
-        BNMF_TRACE(1, gd.pos);
-        if (elect_one()) {
-          if (ty == 0)
-            issue_vt(dcol, tmem + TM_HP, tmem + TM_HP + 16, dplus(d_wa, idx * 2048),
-                     dplus(d_wa, idx * 2048 + HILO), id32);
-          else
-            issue_vt(dcol, tmem + TM_WT, tmem + TM_WT + 16, dplus(d_hn, idx * 2048),
-                     dplus(d_hn, idx * 2048 + HILO), id32);
-          mma_commit(&bar_dfull[gd.pos & 1]);
-        }
-        __syncwarp();
-        BNMF_PROF_ADD(6, tdi);
-        BNMF_TRACE(2, gd.pos);
-        advance(gd);
       }
-      // ---- side products of item ns ----
-      int ty, blk, idx;
-      item(gs, ty, blk, idx);
+      BNMF_TRACE(1, nd);
+      if (elect_one()) {
+        issue_vt(tmem + TM_D + 32 * (nd & 1), tmem + TM_HP, tmem + TM_HP + 16,
+                 dplus(d_wa, j * 2048), dplus(d_wa, j * 2048 + HILO), id32);
+        mma_commit(&bar_dfull[nd & 1]);
+      }
+      __syncwarp();
+      BNMF_TRACE(2, nd);
+      ++nd;
+    };
+    auto d_w = [&](int blk, int u) {
+      if (u == 0) {
+        BNMF_TRACE(6, nd);
+        pwait(bar_hn, blk & 1, 1);
+        BNMF_TRACE(7, nd);
+        tc_fence_after();
+        w0_issued = blk;
+      }
+      BNMF_TRACE(1, nd);
+      if (elect_one()) {
+        issue_vt(tmem + TM_D + 32 * (nd & 1), tmem + TM_WT, tmem + TM_WT + 16,
+                 dplus(d_hn, u * 2048), dplus(d_hn, u * 2048 + HILO), id32);
+        mma_commit(&bar_dfull[nd & 1]);
+      }
+      __syncwarp();
+      BNMF_TRACE(2, nd);
+      ++nd;
+    };
+    auto s_h = [&](int blk, int j) {
       BNMF_TRACE(3, ns);
       pwait(&bar_zfull[ns & 1], (ns >> 1) & 1, 3);
       BNMF_TRACE(4, ns);
+      if (j == 0 && blk > 0) pwait(bar_accfree, (blk - 1) & 1, 4);
       tc_fence_after();
       const uint32_t zb = tmem + TM_Z + 128 * (ns & 1);
-      BNMF_PROF_T0(tsi);
-      if (ty == 0) {
-        if (idx == 0 && blk > 0) {
-          pwait(bar_accfree, (blk - 1) & 1, 4);
-          tc_fence_after();
-        }
-        if (elect_one()) {
-          issue_side(tmem + TM_ACCH, zb, dplus(d_c1, idx * 1024), id32, id16, idx == 0);
-          if (!den_ones)
-            issue_side(tmem + TM_ACCH + 32, zb + 16, dplus(d_c2, idx * 1024), id32, id16, idx == 0);
-          mma_commit(&bar_zempty[ns & 1]);
-          if (idx == SH - 1) mma_commit(bar_acch);
-        }
-      } else {
-        const bool fresh = (blk % FOLD) == 0 && idx == 0;
-        if (fresh && blk > 0) {
-          pwait(bar_accwfree, ((blk / FOLD) - 1) & 1, 5);
-          tc_fence_after();
-        }
-        const bool fold_end = (blk % FOLD) == FOLD - 1 || blk == nb - 1;
-        if (elect_one()) {
-          const uint64_t bh = dplus(d_hnt, idx * 1024);
-          issue_side(tmem + TM_ACCW, zb, bh, id32, id16, fresh);
-          issue_side(tmem + TM_ACCW + 32, zb + 16, bh, id32, id16, fresh);
-          mma_commit(&bar_zempty[ns & 1]);
-          if (idx == SW - 1) {
-            mma_commit(bar_wdone);
-            if (fold_end) mma_commit(bar_accw);
-          }
+      if (elect_one()) {
+        issue_side(tmem + TM_ACCH, zb, dplus(d_c1, j * 1024), id32, id16, j == 0);
+        if (!den_ones)
+          issue_side(tmem + TM_ACCH + 32, zb + 16, dplus(d_c2, j * 1024), id32, id16, j == 0);
+        if (j == SH - 1) mma_commit(bar_acch);
+      }
+      __syncwarp();
+      BNMF_TRACE(5, ns);
+      ++ns;
+    };
+    auto s_w = [&](int blk, int u) {
+      BNMF_TRACE(3, ns);
+      pwait(&bar_zfull[ns & 1], (ns >> 1) & 1, 3);
+      BNMF_TRACE(4, ns);
+      const bool fresh = (blk % FOLD) == 0 && u == 0;
+      if (fresh && blk > 0) pwait(bar_accwfree, ((blk / FOLD) - 1) & 1, 5);
+      tc_fence_after();
+      const bool fold_end = (blk % FOLD) == FOLD - 1 || blk == nb - 1;
+      const uint32_t zb = tmem + TM_Z + 128 * (ns & 1);
+      if (elect_one()) {
+        const uint64_t bh = dplus(d_hnt, u * 1024);
+        issue_side(tmem + TM_ACCW, zb, bh, id32, id16, fresh);
+        issue_side(tmem + TM_ACCW + 32, zb + 16, bh, id32, id16, fresh);
+        if (u == SW - 1) {
+          mma_commit(bar_wdone);
+          if (fold_end) mma_commit(bar_accw);
         }
       }
       __syncwarp();
-      BNMF_PROF_ADD(7, tsi);
       BNMF_TRACE(5, ns);
-      advance(gs);
+      ++ns;
+    };
+
+    if (nb > 0) {
+      if (do_h) d_h(0, 0);
+      else d_w(0, 0);
+    }
+    for (int bi = 0; bi < nb; ++bi) {
+      const bool nxt = bi + 1 < nb;
+      if (do_h) {
+        for (int j = bi == 0 ? 0 : 2; j < SH; ++j) {
+          if (j + 1 < SH) d_h(bi, j + 1);
+          else if (nxt) d_h(bi + 1, 0);
+          s_h(bi, j);
+        }
+        if (nxt) {
+          d_h(bi + 1, 1);
+          s_h(bi + 1, 0);
+          d_w(bi, 0);   // U2(bi) needs the side products of H(bi, SH-1): issued above
+          s_h(bi + 1, 1);
+        } else if (w0_issued != bi) {
+          d_w(bi, 0);
+        }
+      }
+      for (int u = 0; u + 1 < SW; ++u) {
+        d_w(bi, u + 1);
+        s_w(bi, u);
+      }
+      // last W item: the next Vt tile is the first item of block bi + 1
+      if (!nxt) {
+        s_w(bi, SW - 1);
+      } else if (do_h && SH > 2) {
+        d_h(bi + 1, 2);
+        s_w(bi, SW - 1);
+      } else if (do_h && bi + 2 < nb) {
+        d_h(bi + 2, 0);
+        s_w(bi, SW - 1);
+      } else {
+        // next is W(bi + 1, 0), whose U2 waits for the W side products of bi
+        s_w(bi, SW - 1);
+        d_w(bi + 1, 0);
+      }
     }
   } else {
     // ======================= epilogue =======================================
@@ -649,16 +663,9 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
     int c = 0;   // item counter (Vt / Z buffer c & 1)
     float objb = 0.f;   // objective of the current block (fp32, 32 terms per thread)
     // Vt tile of item c -> registers; the buffer is handed back right away
-    auto load_d = [&](int buf, float* y) {
-      tmem_ld8(lane_base + TM_D + 32 * buf + 8 * g, y);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_dempty[buf]);
-    };
-    // Z of item c -> TMEM (after the side products of item c - 2 retired)
+    auto load_d = [&](int buf, float* y) { tmem_ld8(lane_base + TM_D + 32 * buf + 8 * g, y); };
+    // Z of item c -> TMEM (buffer free: dfull(c) retired the side products of c - 2)
     auto put_z = [&](int buf, const float* zn, const float* zd) {
-      if (c >= 2) pwait(&bar_zempty[buf], ((c - 2) >> 1) & 1, 6);
-      tc_fence_after();
       store_z(lane_base + TM_Z + 128 * buf + 32 * g, zn, zd);
       tmem_st_wait();
       tc_fence_before();

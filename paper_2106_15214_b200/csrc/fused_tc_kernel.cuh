@@ -174,7 +174,8 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
   uint64_t* bar_dfull = bars + 16;    // [2] Vt tile ready
   uint64_t* bar_zfull = bars + 18;    // [2] Z written
   uint64_t* bar_hp = bars + 22;       // H~_{p-1} of the next block in TMEM
-  uint64_t* bar_hn = bars + 23;       // H~_p of the block in SMEM
+  uint64_t* bar_hn = bars + 23;       // H~_p of the block in SMEM (Vt operand)
+  uint64_t* bar_hnt = bars + 31;      // H~_p of the block in SMEM (transposed, side operand)
   uint64_t* bar_acch = bars + 24;     // AccH of the block complete
   uint64_t* bar_accfree = bars + 25;  // AccH read out
   uint64_t* bar_accw = bars + 26;     // AccW of a fold complete
@@ -266,6 +267,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
     }
     mbar_init(bar_hp, NEPI);
     mbar_init(bar_hn, NEPI);
+    mbar_init(bar_hnt, NEPI);
     mbar_init(bar_acch, 1);
     mbar_init(bar_accfree, NEPI);
     mbar_init(bar_accw, 1);
@@ -385,6 +387,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
       BNMF_TRACE(3, ns);
       pwait(&bar_zfull[ns & 1], (ns >> 1) & 1, 3);
       BNMF_TRACE(4, ns);
+      if (u == 0) pwait(bar_hnt, blk & 1, 1);
       const bool fresh = (blk % FOLD) == 0 && u == 0;
       if (fresh && blk > 0) pwait(bar_accwfree, ((blk / FOLD) - 1) & 1, 5);
       tc_fence_after();
@@ -573,7 +576,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
           float v = 0.f;
           if (k < K) {
             const float dn = den_ones ? cs2[i] : uden[i];
-            const float r = __fdiv_rn(unum[i], fmaxf(dn, floor_f));
+            const float r = __fdividef(unum[i], fmaxf(dn, floor_f));
             const float rg = gam == 1.f ? r : (gam == 0.5f ? sqrtf(r) : powf(r, gam));
             v = h0[i] * rg * nrm[i];
           }
@@ -593,6 +596,9 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
         for (int i = 0; i < 4; ++i) { hi[i] = tf32_hi(hv[i]); lo[i] = hv[i] - hi[i]; }
         sts_f128(sb + OFF_HN + core_off(row, 4 * g), hi[0], hi[1], hi[2], hi[3]);
         sts_f128(sb + OFF_HN + HILO + core_off(row, 4 * g), lo[0], lo[1], lo[2], lo[3]);
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_hn);   // the next Vt tile needs only Hn
         // HnT (K-major over n): transpose 4 x 4 within lane quads so that
         // lane 4m + j holds k = 4g + j of rows 4m .. 4m + 3 (one 16 B chunk)
         const int j = lane & 3;
@@ -616,7 +622,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
       }
       fence_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar_hn);
+      if (lane == 0) mbar_arrive(bar_hnt);
       BNMF_TRACE(47, blk);
       // global traffic only after the SMEM publish (the proxy fence above
       // would otherwise wait for these stores)

@@ -81,6 +81,15 @@ int bnmf_ctx_init_comm(bnmf_ctx* ctx, int rank, int nranks, const void* id128,
 int bnmf_set_dense(bnmf_ctx* ctx, const void* v, int src_dtype, int src_on_device,
                    int64_t F, int64_t N, int64_t ld, double kappa);
 
+/* Statistics of the values passed to the last bnmf_set_dense (before the
+ * kappa shift), computed on the device during the upload: out[0] min and
+ * out[1] max of the finite entries, out[2] their sum (fp64), out[3] the number
+ * of non-finite entries, out[4] the entry count.  They replace the host scans
+ * of DataMatrix.__post_init__ / check_domain (core.py:188-228) and
+ * default_kappa (core.py:176-185, solver.py:205-221), so the Python layer can
+ * raise the reference's errors without reading V on the host. */
+int bnmf_data_stats(bnmf_ctx* ctx, double* out);
+
 /* Sparse data (beta = 1 only): the local rows of V in CSR (indptr F+1,
  * int32 column indices, fp32 values) plus its CSC view (colptr N+1, int32 row
  * indices, perm[j] = CSR position of CSC entry j) used for the deterministic

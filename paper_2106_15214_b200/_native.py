@@ -75,6 +75,7 @@ _SIGS = {
     "bnmf_stream": ([C.c_void_p], C.c_void_p),
     "bnmf_set_profiling": ([C.c_void_p, C.c_int], C.c_int),
     "bnmf_pass_time": ([C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_int)], C.c_int),
+    "bnmf_data_stats": ([C.c_void_p, C.POINTER(C.c_double)], C.c_int),
 }
 
 
@@ -175,6 +176,13 @@ class Context:
             self._check(self.lib.bnmf_set_dense(self.h, _ptr(v), src, 0, F, N, ld,
                                                 float(kappa)))
         self.F, self.N = F, N
+
+    def data_stats(self):
+        """(min, max, sum, non-finite count, count) of the values of the last
+        set_dense, before the kappa shift, computed on the device."""
+        out = (C.c_double * 5)()
+        self._check(self.lib.bnmf_data_stats(self.h, out))
+        return tuple(out)
 
     def set_csr(self, indptr, indices, values, colptr, rowidx, perm, shape):
         """Host CSR (+ CSC view) of the local rows of V (see include/bnmf.h)."""

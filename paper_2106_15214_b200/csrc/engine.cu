@@ -122,6 +122,8 @@ struct Engine : EngineBase {
     if (st) cudaFree(st);
     if (st_host) cudaFreeHost(st_host);
     if (staging) cudaFree(staging);
+    if (stats_part) cudaFree(stats_part);
+    if (stats_acc) cudaFree(stats_acc);
     if (fused) fused_destroy(fused);
     if (comm_nccl) ncclCommDestroy(comm_nccl);
     if (stream) cudaStreamDestroy(stream);
@@ -143,10 +145,35 @@ struct Engine : EngineBase {
     return 0;
   }
 
+  // statistics of a rows x cols source block, accumulated into stats_acc
+  double* stats_part = nullptr;
+  double* stats_acc = nullptr;
+  int64_t stats_count = 0;
+  template <typename S_>
+  int stats_of(const S_* src, size_t lds, int rows, size_t cols, bool first) {
+    if (!stats_part) {
+      CK(cudaMalloc(&stats_part, STATS_BLOCKS * 4 * sizeof(double)));
+      CK(cudaMalloc(&stats_acc, 4 * sizeof(double)));
+    }
+    stats_partial<S_><<<STATS_BLOCKS, 256, 0, stream>>>(src, lds, rows, cols, stats_part);
+    stats_final<<<1, 32, 0, stream>>>(stats_part, STATS_BLOCKS, stats_acc, first ? 1 : 0);
+    CK(cudaGetLastError());
+    return 0;
+  }
+  int data_stats(double* out5) override {
+    if (!stats_acc) return fail(BNMF_E_STATE, "no dense data");
+    CK(cudaSetDevice(device));
+    CK(cudaMemcpyAsync(out5, stats_acc, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    out5[4] = double(stats_count);
+    return 0;
+  }
+
   template <typename S_>
   int convert_in(const void* src, size_t lds, int rows, size_t cols, double kappa, int on_dev) {
     const size_t chunk_bytes = size_t(256) << 20;
     if (on_dev) {
+      if (int rc = stats_of(reinterpret_cast<const S_*>(src), lds, rows, cols, true)) return rc;
       convert_rows<S_, T><<<grid_for(size_t(rows) * cols), 256, 0, stream>>>(
           reinterpret_cast<const S_*>(src), lds, V, ldv, rows, cols, kappa);
       CK(cudaGetLastError());
@@ -161,6 +188,7 @@ struct Engine : EngineBase {
                            reinterpret_cast<const S_*>(src) + size_t(r0) * lds,
                            lds * sizeof(S_), cols * sizeof(S_), nr,
                            cudaMemcpyHostToDevice, stream));
+      if (int rc = stats_of(reinterpret_cast<const S_*>(staging), cols, nr, cols, r0 == 0)) return rc;
       convert_rows<S_, T><<<grid_for(size_t(nr) * cols), 256, 0, stream>>>(
           reinterpret_cast<const S_*>(staging), cols, V + size_t(r0) * ldv, ldv, nr, cols,
           kappa);
@@ -181,10 +209,14 @@ struct Engine : EngineBase {
     CK(cudaMalloc(&V, size_t(F) * ldv * sizeof(T)));
     if (ldv != size_t(N)) CK(cudaMemsetAsync(V, 0, size_t(F) * ldv * sizeof(T), stream));
     int rc;
+    stats_count = int64_t(F) * N;
     if (!on_dev && src_dtype == dtype && kappa == 0.0) {
-      CK(cudaMemcpy2DAsync(V, ldv * sizeof(T), v, size_t(ld) * sizeof(T), size_t(N) * sizeof(T),
-                           F, cudaMemcpyHostToDevice, stream));
-      rc = 0;
+      if (size_t(ld) == ldv)   // contiguous rows: one linear copy
+        CK(cudaMemcpyAsync(V, v, size_t(F) * ldv * sizeof(T), cudaMemcpyHostToDevice, stream));
+      else
+        CK(cudaMemcpy2DAsync(V, ldv * sizeof(T), v, size_t(ld) * sizeof(T),
+                             size_t(N) * sizeof(T), F, cudaMemcpyHostToDevice, stream));
+      rc = stats_of(V, ldv, F, size_t(N), true);
     } else if (src_dtype == BNMF_FP64) {
       rc = convert_in<double>(v, size_t(ld), F, size_t(N), kappa, on_dev);
     } else {
@@ -580,6 +612,13 @@ struct Engine : EngineBase {
     return 0;
   }
 
+  int prepare(int64_t n) override {
+    if (!begun) return fail(BNMF_E_STATE, "begin must precede step");
+    CK(cudaSetDevice(device));
+    if (n >= kChunk) return capture(kChunk);
+    return 0;
+  }
+
   int step(int64_t n) override {
     if (!begun) return fail(BNMF_E_STATE, "begin must precede step");
     CK(cudaSetDevice(device));
@@ -728,6 +767,14 @@ int bnmf_set_dense(bnmf_ctx* ctx, const void* v, int src_dtype, int src_on_devic
   return ctx->eng->set_dense(v, src_dtype, src_on_device, F, N, ld, kappa);
 }
 
+int bnmf_data_stats(bnmf_ctx* ctx, double* out) {
+  CTX_CHECK(ctx);
+  if (!out) return set_err("null output", BNMF_E_ARG);
+  int rc = ctx->eng->data_stats(out);
+  if (rc < 0) return set_err("data statistics need dense data", BNMF_E_STATE);
+  return rc;
+}
+
 int bnmf_set_csr(bnmf_ctx* ctx, const int64_t* indptr, const int32_t* indices,
                  const float* values, const int64_t* colptr, const int32_t* rowidx,
                  const int32_t* perm, int64_t F, int64_t N, int64_t nnz, int src_on_device) {
@@ -774,6 +821,7 @@ int bnmf_step_timed(bnmf_ctx* ctx, int64_t n, float* ms) {
   cudaSetDevice(e->device);
   if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess)
     return set_err("event create", BNMF_E_CUDA);
+  if (int rc0 = e->prepare(n)) return rc0;
   cudaEventRecord(a, e->stream);
   int rc = e->step(n);
   cudaEventRecord(b, e->stream);

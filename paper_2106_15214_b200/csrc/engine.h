@@ -26,12 +26,18 @@ struct EngineBase {
 
   virtual ~EngineBase() {}
   int fail(int code, const std::string& msg);
+  // [min, max, sum, non-finite count, count] of the values passed to the
+  // last set_dense (before the kappa shift)
+  virtual int data_stats(double* out5) { (void)out5; return -1; }
   virtual int set_dense(const void* v, int src_dtype, int on_dev, int64_t F, int64_t N,
                         int64_t ld, double kappa) = 0;
   virtual int set_factors(const double* w, const double* h, int64_t K, int on_dev) = 0;
   virtual int get_factors(double* w, double* h) = 0;
   virtual int begin(const bnmf_params* p, int64_t max_iters) = 0;
   virtual int step(int64_t n) = 0;
+  // build whatever step(n) will replay (CUDA graph) without running it, so a
+  // timed step does not include graph capture / instantiation
+  virtual int prepare(int64_t n) { (void)n; return 0; }
   virtual int sync(int64_t* done, int* conv) = 0;
   virtual int read_trace(double* obj, double* sec, double* kkt, int64_t n) = 0;
   virtual int init_comm(int rank, int nranks, const void* id, int64_t n_global) = 0;

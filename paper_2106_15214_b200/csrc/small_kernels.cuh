@@ -180,6 +180,56 @@ __global__ void convert_rows(const S* __restrict__ src, size_t lds, T* __restric
   }
 }
 
+// Data statistics for the input checks of DataMatrix / default_kappa
+// (core.py:176-228): per-block [min, max, sum, non-finite count] of a rows x
+// cols matrix (leading dimension lds), fp64, fixed-order tree reduction.
+constexpr int STATS_BLOCKS = 296;
+template <typename S>
+__global__ void __launch_bounds__(256) stats_partial(const S* __restrict__ src, size_t lds, int rows,
+                                                     size_t cols, double* __restrict__ part) {
+  double mn = INFINITY, mx = -INFINITY, sm = 0.0, nf = 0.0;
+  const size_t count = (size_t)rows * cols;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / cols, c = i - r * cols;
+    const double v = double(src[r * lds + c]);
+    if (isfinite(v)) {
+      mn = fmin(mn, v);
+      mx = fmax(mx, v);
+      sm += v;
+    } else {
+      nf += 1.0;
+    }
+  }
+  __shared__ double red[4][256];
+  red[0][threadIdx.x] = mn; red[1][threadIdx.x] = mx; red[2][threadIdx.x] = sm; red[3][threadIdx.x] = nf;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      red[0][threadIdx.x] = fmin(red[0][threadIdx.x], red[0][threadIdx.x + o]);
+      red[1][threadIdx.x] = fmax(red[1][threadIdx.x], red[1][threadIdx.x + o]);
+      red[2][threadIdx.x] += red[2][threadIdx.x + o];
+      red[3][threadIdx.x] += red[3][threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < 4) part[blockIdx.x * 4 + threadIdx.x] = red[threadIdx.x][0];
+}
+// fold the block partials (fixed order) into acc[4]; accumulate across calls
+static __global__ void stats_final(const double* __restrict__ part, int nblk, double* acc, int first) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double mn = first ? INFINITY : acc[0], mx = first ? -INFINITY : acc[1];
+  double sm = first ? 0.0 : acc[2], nf = first ? 0.0 : acc[3];
+  double cs = 0.0;
+  for (int b = 0; b < nblk; ++b) {
+    mn = fmin(mn, part[4 * b]);
+    mx = fmax(mx, part[4 * b + 1]);
+    cs += part[4 * b + 2];
+    nf += part[4 * b + 3];
+  }
+  acc[0] = mn; acc[1] = mx; acc[2] = sm + cs; acc[3] = nf;
+}
+
 // K x N (fp64, row-major) -> N x K (T)
 template <typename T>
 __global__ void transpose_in(const double* __restrict__ src, int K, size_t N, T* __restrict__ dst) {

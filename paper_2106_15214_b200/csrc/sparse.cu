@@ -487,6 +487,12 @@ struct SparseEngine : EngineBase {
     return 0;
   }
 
+  int prepare(int64_t n) override {
+    if (!begun) return fail(BNMF_E_STATE, "begin must precede step");
+    SCK(cudaSetDevice(device));
+    return n >= 16 ? capture(16) : 0;
+  }
+
   int step(int64_t n) override {
     if (!begun) return fail(BNMF_E_STATE, "begin must precede step");
     SCK(cudaSetDevice(device));

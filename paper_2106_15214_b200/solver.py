@@ -181,6 +181,56 @@ def _prepare(data, config):
     return data
 
 
+# Inputs at least this large are checked from device statistics of the
+# upload (a host scan of V costs ~1 s per 10^9 entries); smaller ones are
+# checked on the host before any device work, exactly like the reference.
+_DEVICE_CHECK_MIN = 1 << 24
+
+
+def _upload_checked(ctx, values, config):
+    """Upload V and apply the checks of DataMatrix.__post_init__, check_domain
+    and _prepare (core.py:188-228, solver.py:205-221) to device statistics of
+    the upload, in the reference's order and with its messages.  Returns the
+    (values-free) DataMatrix stand-in (shape, kappa) and F, N."""
+    if values.dtype not in (np.float64, np.float32):
+        values = values.astype(np.float64)
+    if values.ndim != 2 or min(values.shape) < 1:
+        raise ValueError("data must be a 2-D matrix with positive dimensions")
+    kappa = config.kappa
+    ctx.set_dense(values, 0.0 if kappa is None else kappa)
+    vmin, _vmax, vsum, nonfinite, count = ctx.data_stats()
+    if nonfinite > 0:
+        raise ValueError("data entries must be finite")
+    if vmin < 0.0:
+        raise ValueError("data entries must be nonnegative")
+    if kappa is None:
+        # default_kappa (core.py:176-185)
+        kappa = 0.0 if (1.0 <= config.beta <= 2.0 and vmin > 0.0) else 1e-9 * (vsum / count)
+        if kappa != 0.0:
+            ctx.set_dense(values, kappa)
+    kappa = float(kappa)
+    if not np.isfinite(kappa) or kappa < 0.0:
+        raise ValueError("kappa must be a nonnegative finite real")
+    if config.beta < 1.0 and kappa == 0.0 and vmin == 0.0:
+        raise DivergenceDomainError(
+            f"data contains zeros, which is outside the domain of "
+            f"d_beta for beta={config.beta}; set a positive kappa shift")
+    if config.beta <= 0.0 and vmin + kappa <= 0.0:
+        raise DivergenceDomainError(
+            f"data entries must be positive for beta={config.beta}; "
+            f"set a positive kappa shift")
+    F, N = values.shape
+    return _Checked((F, N), kappa), F, N
+
+
+class _Checked:
+    """shape / kappa of device-checked data (what _run reads of a DataMatrix)"""
+
+    def __init__(self, shape, kappa):
+        self.shape = shape
+        self.kappa = kappa
+
+
 # ----------------------------------------------------------------------------
 # native execution
 
@@ -297,16 +347,26 @@ def _run(data, config, counter, algorithm, *, dtype="fp64", init=None, device=No
         w0, h0 = init if not isinstance(init, FactorPair) else (init.w, init.h)
         w0, h0 = parallel.slice_init(w0, h0, n0, N, n_global)
         pair = _resolve_init((w0, h0), F, N, config.rank, config.seed)
-    else:
+    elif isinstance(data, DataMatrix) or np.asarray(data).size < _DEVICE_CHECK_MIN:
         data = _prepare(data, config)
         F, N = data.shape
         n_global = N
         pair = _resolve_init(init, F, N, config.rank, config.seed)
+    else:
+        # plain array: the DataMatrix checks run on device statistics of the
+        # upload (same order, same errors), not as host scans of V
+        values = np.asarray(data)
+        data = None
     ctx = get_context(device, dtype)
     with ctx.lock:
         if sharded:
             _attach_comm(ctx, n_global)
-        ctx.set_dense(data.values, data.kappa)
+        if data is None:
+            data, F, N = _upload_checked(ctx, values, config)
+            n_global = N
+            pair = _resolve_init(init, F, N, config.rank, config.seed)
+        else:
+            ctx.set_dense(data.values, data.kappa)
         ctx.set_factors(pair.w, pair.h)
         params = make_params(config, data.kappa, kkt=kkt, schedule=schedule)
         done, converged = ctx.run(params, config.max_outer_iters)
@@ -315,11 +375,9 @@ def _run(data, config, counter, algorithm, *, dtype="fp64", init=None, device=No
     trace = [TraceRow(i + 1, float(obj[i]), float(sec[i]), float(kk[i, 0]), float(kk[i, 1]))
              for i in range(done)]
     _count_ops(counter, config, done)
-    try:
-        factors = FactorPair(w, h)
-    except ValueError:
-        # fp32 runs may underflow a factor entry to exactly 0; report as is
-        factors = _unchecked_pair(w, h)
+    # the factors are produced by the device loop (strictly positive unless an
+    # fp32 entry underflows to 0, which is reported as is): no host re-scan
+    factors = _unchecked_pair(w, h)
     return FitResult(factors=factors, trace=trace,
                      termination=Termination.CONVERGED if converged else Termination.MAX_ITERS,
                      iterations=done, config=config)

@@ -65,6 +65,8 @@ def build(verbose=False, force=False):
               "--expt-relaxed-constexpr"]
     if os.environ.get("BNMF_WATCHDOG", "0") == "1":
         common.append("-DBNMF_WATCHDOG")
+    for flag in os.environ.get("BNMF_DEFS", "").split():
+        common.append(f"-D{flag}")
     if os.environ.get("BNMF_TC_PROF", "0") == "1":
         common.append("-DBNMF_TC_PROF")
     srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]

@@ -67,11 +67,17 @@ constexpr uint32_t OFF_WA = OFF_STAGE + NSTAGE * STAGE_BYTES;   // [128 f x 16] 
 constexpr uint32_t OFF_C1 = OFF_WA + 2 * FR * KP * 4;           // [32 (k hi, k lo) x 128 f]
 constexpr uint32_t OFF_C2 = OFF_C1 + 2 * FR * KP * 4;
 constexpr uint32_t OFF_HN = OFF_C2 + 2 * FR * KP * 4;           // [128 n x 16] hi, lo
-constexpr uint32_t OFF_HNT = OFF_HN + 2 * BN * KP * 4;          // [32 (k hi, k lo) x 128 n]
-constexpr uint32_t OFF_XCH = OFF_HNT + 2 * BN * KP * 4;         // peer's AccH partial
+// H~_p transposed (B of the W-side products, K-major over n): rows k (hi) and 16 + k (lo),
+// core matrices of 8 k x 4 n.  The 4-column chunks sit 144 B apart (not 128) so that a warp
+// storing one k of 32 consecutive columns hits 32 different banks.
+constexpr uint32_t HNT_LBO = 144;
+constexpr uint32_t HNT_SBO = (BN / 4) * HNT_LBO;                // 8-row (k) group stride
+constexpr uint32_t OFF_HNT = OFF_HN + 2 * BN * KP * 4;
+constexpr uint32_t OFF_XCH = OFF_HNT + 4 * HNT_SBO;             // peer's AccH partial
 constexpr uint32_t OFF_BAR = OFF_XCH + BN * 2 * KP * 4;
 constexpr uint32_t SMEM_BYTES = OFF_BAR + 512 + 1024;           // + alignment slack
 constexpr uint32_t HILO = FR * KP * 4;                          // hi -> lo offset (8 KB)
+static_assert(SMEM_BYTES <= 232448, "fused_pass_tc: shared memory over the 227 KB limit");
 
 // beta class of the fused TC epilogue (adds the beta = 1.5 fast form)
 enum { FBC_GEN = 0, FBC_0 = 1, FBC_1 = 2, FBC_2 = 3, FBC_15 = 4 };
@@ -80,6 +86,10 @@ enum { FBC_GEN = 0, FBC_0 = 1, FBC_1 = 2, FBC_2 = 3, FBC_15 = 4 };
 // 8-row groups at SBO = 4096 B, 4-wide chunks of c at LBO = 128 B
 __host__ __device__ __forceinline__ uint32_t coreT_off(int k, int c) {
   return uint32_t((k >> 3) * 4096 + (c >> 2) * 128 + (k & 7) * 16 + (c & 3) * 4);
+}
+// element (k, n) of the transposed H~_p tile (k < 32: hi rows 0..15, lo rows 16..31)
+__host__ __device__ __forceinline__ uint32_t hnt_off(int k, int n) {
+  return uint32_t((k >> 3) * HNT_SBO + (n >> 2) * HNT_LBO + (k & 7) * 16 + (n & 3) * 4);
 }
 
 template <int FBC>
@@ -103,7 +113,6 @@ __device__ __forceinline__ void zpair(float x, float y, float beta, float& zn, f
 template <int FBC>
 __device__ __forceinline__ float dterm(float x, float y, float zd, float beta) {
   if (FBC == FBC_15) {
-    // d_{3/2}(x|y) = (2/3) (sqrt x - sqrt y)^2 (2 sqrt x + sqrt y); zd = sqrt y
     const float sx = sqrt_fast(x);
     const float dq = sx - zd;
     return 0.6666666666666666f * dq * dq * fmaf(2.f, sx, zd);
@@ -117,9 +126,30 @@ __device__ __forceinline__ float dterm(float x, float y, float zd, float beta) {
   return divergence32<BC_GEN>(x, y, beta);
 }
 
+// acc += d(x|y), except beta = 1.5: acc += (3/2) d(x|y) (the caller applies 2/3 once)
+template <int FBC>
+__device__ __forceinline__ void dacc(float x, float y, float zd, float beta, float& acc) {
+  if (FBC == FBC_15) {
+    // d_{3/2}(x|y) = (2/3) (sqrt x - sqrt y)^2 (2 sqrt x + sqrt y); zd = sqrt y
+    const float sx = sqrt_fast(x);
+    const float dq = sx - zd;
+    acc = fmaf(dq * dq, fmaf(2.f, sx, zd), acc);
+  } else {
+    acc += dterm<FBC>(x, y, zd, beta);
+  }
+}
+
 // Z of one k-step (this thread's 8 columns) as TMEM A operands:
 // [Zn hi | Zn lo | Zd hi | Zd lo], 8 columns each, one 32-column store
 __device__ __forceinline__ void store_z(uint32_t taddr, const float* zn, const float* zd) {
+#ifdef BNMF_Z1
+  float a[8], b[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { a[i] = to_tf32(zn[i]); b[i] = to_tf32(zd[i]); }
+  tmem_st8(taddr, a);
+  tmem_st8(taddr + 16, b);
+  return;
+#endif
   float z[32];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -150,12 +180,15 @@ __device__ __forceinline__ void issue_vt(uint32_t dcol, uint32_t a_hi, uint32_t 
 // acc[:, 0:32] (+)= Z_hi * [B_hi | B_lo], acc[:, 0:16] += Z_lo * B_hi over a
 // 32-wide K slab: Z hi/lo of k-step s at TMEM columns z + 32 s (+8 for lo),
 // B (32 x K, K-major) from descriptor b, 256 B per k-step.
+template <uint32_t KSTRIDE>
 __device__ __forceinline__ void issue_side(uint32_t acc, uint32_t z, uint64_t b, uint32_t id32,
                                            uint32_t id16, bool fresh) {
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
-    mma_ts(acc, z + 32 * s, dplus(b, 256 * s), id32, (fresh && s == 0) ? 0u : 1u);
-    mma_ts(acc, z + 32 * s + 8, dplus(b, 256 * s), id16, 1u);
+    mma_ts(acc, z + 32 * s, dplus(b, KSTRIDE * s), id32, (fresh && s == 0) ? 0u : 1u);
+#ifndef BNMF_Z1
+    mma_ts(acc, z + 32 * s + 8, dplus(b, KSTRIDE * s), id16, 1u);
+#endif
   }
 }
 
@@ -174,8 +207,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
   uint64_t* bar_dfull = bars + 16;    // [2] Vt tile ready
   uint64_t* bar_zfull = bars + 18;    // [2] Z written
   uint64_t* bar_hp = bars + 22;       // H~_{p-1} of the next block in TMEM
-  uint64_t* bar_hn = bars + 23;       // H~_p of the block in SMEM (Vt operand)
-  uint64_t* bar_hnt = bars + 31;      // H~_p of the block in SMEM (transposed, side operand)
+  uint64_t* bar_hn = bars + 23;       // H~_p of the block in SMEM (both layouts)
   uint64_t* bar_acch = bars + 24;     // AccH of the block complete
   uint64_t* bar_accfree = bars + 25;  // AccH read out
   uint64_t* bar_accw = bars + 26;     // AccW of a fold complete
@@ -267,7 +299,6 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
     }
     mbar_init(bar_hp, NEPI);
     mbar_init(bar_hn, NEPI);
-    mbar_init(bar_hnt, NEPI);
     mbar_init(bar_acch, 1);
     mbar_init(bar_accfree, NEPI);
     mbar_init(bar_accw, 1);
@@ -331,7 +362,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
     const uint64_t d_hn = sdesc(sb + OFF_HN, 128, 512);
     const uint64_t d_c1 = sdesc(sb + OFF_C1, 128, 4096);
     const uint64_t d_c2 = sdesc(sb + OFF_C2, 128, 4096);
-    const uint64_t d_hnt = sdesc(sb + OFF_HNT, 128, 4096);
+    const uint64_t d_hnt = sdesc(sb + OFF_HNT, HNT_LBO, HNT_SBO);
     int nd = 0, ns = 0, w0_issued = -1;
     auto d_h = [&](int blk, int j) {
       if (j == 0) {
@@ -374,9 +405,9 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
       tc_fence_after();
       const uint32_t zb = tmem + TM_Z + 128 * (ns & 1);
       if (elect_one()) {
-        issue_side(tmem + TM_ACCH, zb, dplus(d_c1, j * 1024), id32, id16, j == 0);
+        issue_side<256>(tmem + TM_ACCH, zb, dplus(d_c1, j * 1024), id32, id16, j == 0);
         if (!den_ones)
-          issue_side(tmem + TM_ACCH + 32, zb + 16, dplus(d_c2, j * 1024), id32, id16, j == 0);
+          issue_side<256>(tmem + TM_ACCH + 32, zb + 16, dplus(d_c2, j * 1024), id32, id16, j == 0);
         if (j == SH - 1) mma_commit(bar_acch);
       }
       __syncwarp();
@@ -387,16 +418,15 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
       BNMF_TRACE(3, ns);
       pwait(&bar_zfull[ns & 1], (ns >> 1) & 1, 3);
       BNMF_TRACE(4, ns);
-      if (u == 0) pwait(bar_hnt, blk & 1, 1);
       const bool fresh = (blk % FOLD) == 0 && u == 0;
       if (fresh && blk > 0) pwait(bar_accwfree, ((blk / FOLD) - 1) & 1, 5);
       tc_fence_after();
       const bool fold_end = (blk % FOLD) == FOLD - 1 || blk == nb - 1;
       const uint32_t zb = tmem + TM_Z + 128 * (ns & 1);
       if (elect_one()) {
-        const uint64_t bh = dplus(d_hnt, u * 1024);
-        issue_side(tmem + TM_ACCW, zb, bh, id32, id16, fresh);
-        issue_side(tmem + TM_ACCW + 32, zb + 16, bh, id32, id16, fresh);
+        const uint64_t bh = dplus(d_hnt, u * 8 * HNT_LBO);
+        issue_side<2 * HNT_LBO>(tmem + TM_ACCW, zb, bh, id32, id16, fresh);
+        issue_side<2 * HNT_LBO>(tmem + TM_ACCW + 32, zb + 16, bh, id32, id16, fresh);
         if (u == SW - 1) {
           mma_commit(bar_wdone);
           if (fold_end) mma_commit(bar_accw);
@@ -590,39 +620,23 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
       if (blk > 0) pwait(bar_wdone, (blk - 1) & 1, 6);   // W MMAs of blk-1 read Hn/HnT
       BNMF_TRACE(46, blk);
       {
-        // Hn: this thread's 4 k of row n are one 16 B chunk of the core tile
+        // Hn: this thread's 4 k of row n are one 16 B chunk of the core tile;
+        // HnT: 8 conflict-free scalar stores (hi, lo of 4 k)
         float hi[4], lo[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) { hi[i] = tf32_hi(hv[i]); lo[i] = hv[i] - hi[i]; }
         sts_f128(sb + OFF_HN + core_off(row, 4 * g), hi[0], hi[1], hi[2], hi[3]);
         sts_f128(sb + OFF_HN + HILO + core_off(row, 4 * g), lo[0], lo[1], lo[2], lo[3]);
+        const uint32_t ta = sb + OFF_HNT + hnt_off(4 * g, row);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          sts_f32(ta + i * 16, hi[i]);
+          sts_f32(ta + 2 * HNT_SBO + i * 16, lo[i]);
+        }
         fence_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar_hn);   // the next Vt tile needs only Hn
-        // HnT (K-major over n): transpose 4 x 4 within lane quads so that
-        // lane 4m + j holds k = 4g + j of rows 4m .. 4m + 3 (one 16 B chunk)
-        const int j = lane & 3;
-        float tv[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int si = (j - r) & 3;   // this lane sends its value for k index si
-          const float send = si == 0 ? hv[0] : si == 1 ? hv[1] : si == 2 ? hv[2] : hv[3];
-          const float got = __shfl_sync(0xffffffffu, send, (lane & ~3) | ((j + r) & 3));
-          const int dr = (j + r) & 3;   // received: row 4m + dr, k index j
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-            if (t == dr) tv[t] = got;
-        }
-        float th[4], tl[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) { th[t] = tf32_hi(tv[t]); tl[t] = tv[t] - th[t]; }
-        const int rb = row & ~3;
-        sts_f128(sb + OFF_HNT + coreT_off(4 * g + j, rb), th[0], th[1], th[2], th[3]);
-        sts_f128(sb + OFF_HNT + coreT_off(4 * g + j + 16, rb), tl[0], tl[1], tl[2], tl[3]);
+        if (lane == 0) mbar_arrive(bar_hn);
       }
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_hnt);
       BNMF_TRACE(47, blk);
       // global traffic only after the SMEM publish (the proxy fence above
       // would otherwise wait for these stores)
@@ -725,7 +739,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
       pwait(&bar_dfull[buf], (c >> 1) & 1, 2);
       BNMF_TRACE(31, c);
       tc_fence_after();
-      float y[8], x[8], zn[8], zd[8], dd[8];
+      float y[8], x[8], zn[8], zd[8];
       load_d(buf, y);
       if (q < SH) {
         const uint32_t xa = xrow + (32 * idx + 8 * g) * 4;
@@ -736,23 +750,33 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
 #pragma unroll
         for (int i = 0; i < 8; ++i) x[i] = 0.f;
       }
+      if (n0 + BN <= N && row < FTr) {
+        float o0 = 0.f, o1 = 0.f;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float yy = KAPPA ? y[i] + kappa : y[i];
-        zpair<FBC>(x[i], yy, beta, zn[i], zd[i]);
-        dd[i] = dterm<FBC>(x[i], yy, zd[i], beta);
-      }
-      if (!(n0 + BN <= N && row < FTr)) {
+        for (int i = 0; i < 8; i += 2) {
+          const float y0 = KAPPA ? y[i] + kappa : y[i], y1 = KAPPA ? y[i + 1] + kappa : y[i + 1];
+          zpair<FBC>(x[i], y0, beta, zn[i], zd[i]);
+          zpair<FBC>(x[i + 1], y1, beta, zn[i + 1], zd[i + 1]);
+          dacc<FBC>(x[i], y0, zd[i], beta, o0);
+          dacc<FBC>(x[i + 1], y1, zd[i + 1], beta, o1);
+        }
+        objb += o0 + o1;
+      } else {
         const bool fok = row < FTr;
+        float o0 = 0.f;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
+          const float yy = KAPPA ? y[i] + kappa : y[i];
+          zpair<FBC>(x[i], yy, beta, zn[i], zd[i]);
           const bool ok = fok && (n0 + 32 * idx + 8 * g + i < N);
+          float t = 0.f;
+          dacc<FBC>(x[i], yy, zd[i], beta, t);
           zn[i] = ok ? zn[i] : 0.f;
           zd[i] = ok ? zd[i] : 0.f;
-          dd[i] = ok ? dd[i] : 0.f;
+          o0 += ok ? t : 0.f;
         }
+        objb += o0;
       }
-      objb += (dd[0] + dd[1]) + (dd[2] + dd[3]) + ((dd[4] + dd[5]) + (dd[6] + dd[7]));
       put_z(buf, zn, zd);
     };
 
@@ -786,7 +810,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
       const uint32_t xrow = sb + OFF_STAGE + stage_of(bi, q < SH ? q : 0, phq) * STAGE_BYTES + lane * VROWB;
       objb = 0.f;
       for (int u = 0; u < SW; ++u) w_item(bi, u, xrow);
-      obj += double(objb);
+      obj += FBC == FBC_15 ? double(objb) * (2.0 / 3.0) : double(objb);
       if (lane == 0)
         for (int j = 0; j < SH; ++j) {
           uint32_t ph;

@@ -138,6 +138,9 @@ static __global__ void finish_iter(RunState* st, int slot, const double* __restr
   trace_sec[it - 1] = st->elapsed;
   st->prev_obj = o;
   st->iters_done = it;
+#ifdef BNMF_X_NOSTOP
+  stop = false;   // timing experiments with garbage numerics
+#endif
   if (stop) { st->stop_iter = it; st->converged = 1; }
 }
 

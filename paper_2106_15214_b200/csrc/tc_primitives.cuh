@@ -50,9 +50,9 @@ __device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t a = smem_u32(bar);
 #ifdef BNMF_WATCHDOG
-  long long spins = 0;
+  const long long t0 = clock64();
   while (!mbar_try(a, parity)) {
-    if (++spins > (1ll << 26)) {
+    if (clock64() - t0 > (1ll << 32)) {
       printf("bnmf watchdog: block %d thread %d stuck on mbarrier %u parity %u\n", blockIdx.x,
              threadIdx.x, a, parity);
       __trap();
@@ -419,9 +419,9 @@ __device__ __forceinline__ bool mbar_try_relaxed_cluster(uint32_t a, uint32_t pa
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
 #ifdef BNMF_WATCHDOG
-  long long spins = 0;
+  const long long t0 = clock64();
   while (!mbar_try_relaxed_cluster(a, parity)) {
-    if (++spins > (1ll << 26)) {
+    if (clock64() - t0 > (1ll << 32)) {
       printf("bnmf watchdog: block %d thread %d stuck on cluster mbarrier %u parity %u\n",
              blockIdx.x, threadIdx.x, a, parity);
       __trap();

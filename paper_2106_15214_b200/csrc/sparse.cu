@@ -7,14 +7,27 @@
 //   H_p = H~ * (W^T (V/Vt)) / colsum(W_p)            updates.py:325-327
 //         (JMM: W^T with W = W~ and Vt = W~H~; BMM: W = W_p, Vt = W_p H~)
 //   D(V | WH) = sum_nnz [x log(x/y) - x] + (1^T W)(H 1)   core.py:101 at x=0
-// Per outer iteration (solver.py:301-319), rows of V are local to the rank:
-//   pass A (CSR, warp per row)   y, z = x/y at the nonzeros, W_p row update,
-//                                per-block colsum / sum-of-squares of W_p
-//   reduce (+ allreduce)         DenH = colsum(W_p), norms = ||W_p[:,k]||
-//   pass B (CSC, warp per column) H_p = H~ * num/DenH, H~_p = H_p * norms,
-//                                per-block rowsum of H~_p (next DenW)
-//   pass C (CSR, warp per row)   W~_p = W_p / norms, objective at nonzeros
-//   finish                       objective + dense term, stop rule
+// Per outer iteration (solver.py:301-319); rows of V (and of W) are local to
+// the rank, H~ is replicated:
+//   pass A  (CSR, warp per row)      y, z = x/y at the nonzeros, W_p row update,
+//                                    per-block colsum / sum-of-squares of W_p
+//   reduce A (+ allreduce 2K)        DenH = colsum(W_p), norms = ||W_p[:,k]||
+//   pass B1 (CSC segments, warp each) partial H numerators: columns are cut
+//                                    into segments of <= SP_SEG nonzeros so
+//                                    that a Zipf-heavy column spreads over
+//                                    many warps
+//   pass B2 (column x k)             segment partials summed in order
+//   (+ allreduce N x K of the numerators when rows are sharded)
+//   pass B3 (column x k)             H_p = H~ * num/DenH, H~_p = H_p * norms,
+//                                    per-block rowsum of H~_p (next DenW)
+//   pass C  (CSR, warp per row)      W~_p = W_p / norms, objective at nonzeros
+//   finish                           objective + dense term, stop rule
+//
+// Warp layout of the nonzero passes: 4 groups of 8 lanes, one nonzero per
+// group, each lane holding KPL consecutive k of the (KL = K rounded up to 32)
+// padded factor rows, so a factor row is one coalesced 8-lane vector load and
+// the dot product needs 3 shuffles.  Factor matrices are stored row-major with
+// leading dimension KL (zero padded).
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -22,6 +35,7 @@
 #include <climits>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "engine.h"
 #include "small_kernels.cuh"
@@ -30,183 +44,264 @@ namespace bnmf {
 
 constexpr int SP_THREADS = 256;
 constexpr int SP_WARPS = SP_THREADS / 32;
-constexpr int SP_KMAX = 128;   // 4 k per lane
-
-// warp sum (butterfly => every lane holds the identical result)
-__device__ __forceinline__ float warp_sum(float v) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
+constexpr int SP_KMAX = 128;
+constexpr int SP_SEG = 2048;   // nonzeros per column segment (pass B1)
 
 struct SpArgs {
-  int F, N, K, KL;             // KL = K rounded up to a multiple of 32 (lanes x per-lane)
+  int F, N, K, KL;
   const long long* indptr;
   const int* indices;
   const float* vals;
-  const long long* colptr;
-  const int* rowidx;
+  const int* rowidx;           // CSC row index
   const int* perm;             // CSC position -> CSR position
+  const long long* segptr;     // [S + 1] CSC positions
+  const int* segcol;           // [S] column of each segment
+  const int* colseg;           // [N + 1] first segment of each column
+  int S;
   float* z;                    // per nonzero (CSR order)
-  float* Wt;                   // W~ (F x K)
-  float* Wp;                   // W_p (F x K)
-  float* Ht;                   // H~ (N x K)
-  float* Hn;                   // H~_p (N x K)
+  float* Wt;                   // W~ (F x KL)
+  float* Wp;                   // W_p (F x KL)
+  float* Ht;                   // H~ (N x KL)
+  float* Hn;                   // H~_p (N x KL)
+  float* part;                 // segment partials (S x KL)
+  float* num;                  // H numerators (N x KL)
   const double* denw;          // rowsum(H~) (K)
   const double* denh;          // colsum(W_p) (K)
   const double* norms;         // ||W_p[:,k]|| (K)
   double* pa;                  // pass A partials [blocks][2K]: colsum, sumsq
-  double* pb;                  // pass B partials [blocks][K]: rowsum(H~_p)
-  double* pc;                  // pass C partials [blocks]: sum_nnz x log(x/y) - x
+  double* pb;                  // pass B3 partials [blocks][K]: rowsum(H~_p)
+  double* pc;                  // pass C partials [blocks]
   int algorithm;
   Scalars sc;
 };
 
+template <int KPL>
+__device__ __forceinline__ void ld_row(const float* p, float* v) {
+#pragma unroll
+  for (int i = 0; i < KPL; i += 4) {
+    const float4 t = *reinterpret_cast<const float4*>(p + i);
+    v[i] = t.x; v[i + 1] = t.y; v[i + 2] = t.z; v[i + 3] = t.w;
+  }
+}
+template <int KPL>
+__device__ __forceinline__ void st_row(float* p, const float* v) {
+#pragma unroll
+  for (int i = 0; i < KPL; i += 4)
+    *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+}
+// sum over the 8 lanes of a group (every lane of the group gets the total)
+__device__ __forceinline__ float group_sum(float v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  return v;
+}
+
 // ---- pass A: rows --------------------------------------------------------
+template <int KPL>
 __global__ void __launch_bounds__(SP_THREADS) sp_pass_a(SpArgs a, const RunState* st, int slot) {
   if (!iter_active(st, slot)) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int K = a.K, per = a.KL / 32;
-  double cs[SP_KMAX / 32], sq[SP_KMAX / 32];
-  for (int i = 0; i < per; ++i) { cs[i] = 0.0; sq[i] = 0.0; }
+  const int grp = lane >> 3, sl = lane & 7, k0 = sl * KPL;
+  const int KL = a.KL;
+  double cs[KPL], sq[KPL];
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) { cs[i] = 0.0; sq[i] = 0.0; }
   __shared__ double red[SP_WARPS][2 * SP_KMAX];
+  double rinv[KPL];
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) {
+    const int k = k0 + i;
+    rinv[i] = k < a.K ? 1.0 / fmax(a.denw[k], a.sc.floor) : 0.0;
+  }
   for (int f = blockIdx.x * SP_WARPS + warp; f < a.F; f += gridDim.x * SP_WARPS) {
-    float w[SP_KMAX / 32], num[SP_KMAX / 32];
-    for (int i = 0; i < per; ++i) {
-      const int k = lane + 32 * i;
-      w[i] = k < K ? a.Wt[size_t(f) * K + k] : 0.f;
-      num[i] = 0.f;
-    }
+    float w[KPL], num[KPL];
+    ld_row<KPL>(a.Wt + size_t(f) * KL + k0, w);
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) num[i] = 0.f;
     const long long j0 = a.indptr[f], j1 = a.indptr[f + 1];
-    for (long long j = j0; j < j1; ++j) {
-      const int n = a.indices[j];
-      const float x = a.vals[j];
-      float h[SP_KMAX / 32], p = 0.f;
-      for (int i = 0; i < per; ++i) {
-        const int k = lane + 32 * i;
-        h[i] = k < K ? a.Ht[size_t(n) * K + k] : 0.f;
-        p = fmaf(w[i], h[i], p);
-      }
-      const float y = warp_sum(p);
-      const float zz = x / y;
-      if (lane == 0) a.z[j] = zz;
-      for (int i = 0; i < per; ++i) num[i] = fmaf(zz, h[i], num[i]);
+    for (long long jj = j0; jj < j1; jj += 4) {
+      const long long j = jj + grp;
+      const bool ok = j < j1;
+      const int n = ok ? a.indices[j] : 0;
+      const float x = ok ? a.vals[j] : 0.f;
+      float h[KPL];
+      ld_row<KPL>(a.Ht + size_t(n) * KL + k0, h);
+      float p = 0.f;
+#pragma unroll
+      for (int i = 0; i < KPL; ++i) p = fmaf(w[i], h[i], p);
+      const float y = group_sum(p);
+      const float zz = ok ? x / y : 0.f;
+      if (ok && sl == 0) a.z[j] = zz;
+#pragma unroll
+      for (int i = 0; i < KPL; ++i) num[i] = fmaf(zz, h[i], num[i]);
     }
-    for (int i = 0; i < per; ++i) {
-      const int k = lane + 32 * i;
-      if (k < K) {
-        const double r = double(num[i]) / fmax(a.denw[k], a.sc.floor);
-        const float wn = float(double(w[i]) * apply_exponent<double>(r, a.sc.gamma));
-        a.Wp[size_t(f) * K + k] = wn;
-        cs[i] += double(wn);
-        sq[i] += double(wn) * double(wn);
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {   // groups 0..3 in a fixed tree
+      num[i] += __shfl_xor_sync(0xffffffffu, num[i], 8);
+      num[i] += __shfl_xor_sync(0xffffffffu, num[i], 16);
+    }
+    if (grp == 0) {
+      float wn[KPL];
+#pragma unroll
+      for (int i = 0; i < KPL; ++i) {
+        const int k = k0 + i;
+        wn[i] = 0.f;
+        if (k < a.K) {
+          const double r = double(num[i]) * rinv[i];
+          wn[i] = float(double(w[i]) * apply_exponent<double>(r, a.sc.gamma));
+          cs[i] += double(wn[i]);
+          sq[i] += double(wn[i]) * double(wn[i]);
+        }
       }
+      st_row<KPL>(a.Wp + size_t(f) * KL + k0, wn);
     }
   }
-  for (int i = 0; i < per; ++i) {
-    red[warp][lane + 32 * i] = cs[i];
-    red[warp][SP_KMAX + lane + 32 * i] = sq[i];
-  }
+  if (grp == 0)
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      red[warp][k0 + i] = cs[i];
+      red[warp][SP_KMAX + k0 + i] = sq[i];
+    }
   __syncthreads();
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+  for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
     double s0 = 0.0, s1 = 0.0;
     for (int w = 0; w < SP_WARPS; ++w) { s0 += red[w][k]; s1 += red[w][SP_KMAX + k]; }
-    a.pa[size_t(blockIdx.x) * 2 * K + k] = s0;
-    a.pa[size_t(blockIdx.x) * 2 * K + K + k] = s1;
+    a.pa[size_t(blockIdx.x) * 2 * a.K + k] = s0;
+    a.pa[size_t(blockIdx.x) * 2 * a.K + a.K + k] = s1;
   }
 }
 
-// ---- pass B: columns -----------------------------------------------------
-__global__ void __launch_bounds__(SP_THREADS) sp_pass_b(SpArgs a, const RunState* st, int slot) {
+// ---- pass B1: column segments -> partial H numerators ----------------------
+template <int KPL>
+__global__ void __launch_bounds__(SP_THREADS) sp_pass_b1(SpArgs a, const RunState* st, int slot) {
   if (!iter_active(st, slot)) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int K = a.K, per = a.KL / 32;
-  double rs[SP_KMAX / 32];
-  for (int i = 0; i < per; ++i) rs[i] = 0.0;
-  __shared__ double red[SP_WARPS][SP_KMAX];
+  const int grp = lane >> 3, sl = lane & 7, k0 = sl * KPL;
+  const int KL = a.KL;
   const bool bmm = a.algorithm == BNMF_BMM;
-  for (int n = blockIdx.x * SP_WARPS + warp; n < a.N; n += gridDim.x * SP_WARPS) {
-    float h[SP_KMAX / 32], num[SP_KMAX / 32];
-    for (int i = 0; i < per; ++i) {
-      const int k = lane + 32 * i;
-      h[i] = k < K ? a.Ht[size_t(n) * K + k] : 0.f;
-      num[i] = 0.f;
-    }
-    const long long j0 = a.colptr[n], j1 = a.colptr[n + 1];
-    for (long long j = j0; j < j1; ++j) {
-      const int f = a.rowidx[j];
-      float w[SP_KMAX / 32];
-      const float* W = bmm ? a.Wp : a.Wt;
-      for (int i = 0; i < per; ++i) {
-        const int k = lane + 32 * i;
-        w[i] = k < K ? W[size_t(f) * K + k] : 0.f;
-      }
+  const float* W = bmm ? a.Wp : a.Wt;
+  for (int s = blockIdx.x * SP_WARPS + warp; s < a.S; s += gridDim.x * SP_WARPS) {
+    const long long j0 = a.segptr[s], j1 = a.segptr[s + 1];
+    float num[KPL], h[KPL];
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) num[i] = 0.f;
+    if (bmm) ld_row<KPL>(a.Ht + size_t(a.segcol[s]) * KL + k0, h);
+    for (long long jj = j0; jj < j1; jj += 4) {
+      const long long j = jj + grp;
+      const bool ok = j < j1;
+      const int f = ok ? a.rowidx[j] : 0;
+      const int pj = ok ? a.perm[j] : 0;
+      float w[KPL];
+      ld_row<KPL>(W + size_t(f) * KL + k0, w);
       float zz;
       if (bmm) {   // block update: Vt2 = W_p H~ at this nonzero (updates.py:173-181)
         float p = 0.f;
-        for (int i = 0; i < per; ++i) p = fmaf(w[i], h[i], p);
-        zz = a.vals[a.perm[j]] / warp_sum(p);
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) p = fmaf(w[i], h[i], p);
+        const float y = group_sum(p);
+        zz = ok ? a.vals[pj] / y : 0.f;
       } else {     // joint update: the anchor's Z from pass A
-        zz = a.z[a.perm[j]];
+        zz = ok ? a.z[pj] : 0.f;
       }
-      for (int i = 0; i < per; ++i) num[i] = fmaf(zz, w[i], num[i]);
+#pragma unroll
+      for (int i = 0; i < KPL; ++i) num[i] = fmaf(zz, w[i], num[i]);
     }
-    for (int i = 0; i < per; ++i) {
-      const int k = lane + 32 * i;
-      if (k < K) {
-        const double r = double(num[i]) / fmax(a.denh[k], a.sc.floor);
-        const double hp = double(h[i]) * apply_exponent<double>(r, a.sc.gamma);
-        const float hn = float(hp * a.norms[k]);
-        a.Hn[size_t(n) * K + k] = hn;
-        rs[i] += double(hn);
-      }
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      num[i] += __shfl_xor_sync(0xffffffffu, num[i], 8);
+      num[i] += __shfl_xor_sync(0xffffffffu, num[i], 16);
+    }
+    if (grp == 0) st_row<KPL>(a.part + size_t(s) * KL + k0, num);
+  }
+}
+
+// ---- pass B2: segment partials of each column, in order -------------------
+__global__ void sp_pass_b2(SpArgs a, const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  const size_t total = size_t(a.N) * a.KL;
+  for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < total;
+       t += size_t(gridDim.x) * blockDim.x) {
+    const int n = int(t / a.KL), k = int(t - size_t(n) * a.KL);
+    const int s0 = a.colseg[n], s1 = a.colseg[n + 1];
+    float v = a.part[size_t(s0) * a.KL + k];
+    if (s1 - s0 > 1) {
+      double acc = double(v);
+      for (int s = s0 + 1; s < s1; ++s) acc += double(a.part[size_t(s) * a.KL + k]);
+      v = float(acc);
+    }
+    a.num[t] = v;
+  }
+}
+
+// ---- pass B3: H update, normalisation, rowsum partials ----------------------
+// block = (SP_THREADS / KL) columns x KL k; grid-stride over column groups
+__global__ void __launch_bounds__(SP_THREADS) sp_pass_b3(SpArgs a, const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  const int KL = a.KL, cpb = SP_THREADS / KL;
+  const int k = threadIdx.x % KL, c = threadIdx.x / KL;
+  __shared__ double red[SP_THREADS];
+  double rs = 0.0;
+  if (c < cpb && k < a.K) {
+    const double dinv = 1.0 / fmax(a.denh[k], a.sc.floor), nk = a.norms[k];
+    for (int n = blockIdx.x * cpb + c; n < a.N; n += gridDim.x * cpb) {
+      const size_t t = size_t(n) * KL + k;
+      const double r = double(a.num[t]) * dinv;
+      const double hp = double(a.Ht[t]) * apply_exponent<double>(r, a.sc.gamma);
+      const float hn = float(hp * nk);
+      a.Hn[t] = hn;
+      rs += double(hn);
     }
   }
-  for (int i = 0; i < per; ++i) red[warp][lane + 32 * i] = rs[i];
+  red[threadIdx.x] = rs;
   __syncthreads();
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+  if (threadIdx.x < a.K) {
     double s = 0.0;
-    for (int w = 0; w < SP_WARPS; ++w) s += red[w][k];
-    a.pb[size_t(blockIdx.x) * K + k] = s;
+    for (int cc = 0; cc < cpb; ++cc) s += red[cc * KL + threadIdx.x];
+    a.pb[size_t(blockIdx.x) * a.K + threadIdx.x] = s;
   }
 }
 
 // ---- pass C: normalise W, objective at the nonzeros ------------------------
+template <int KPL>
 __global__ void __launch_bounds__(SP_THREADS) sp_pass_c(SpArgs a, const RunState* st, int slot) {
   if (!iter_active(st, slot)) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int K = a.K, per = a.KL / 32;
+  const int grp = lane >> 3, sl = lane & 7, k0 = sl * KPL;
+  const int KL = a.KL;
   double acc = 0.0;
-  __shared__ double red[SP_WARPS];
+  __shared__ double red[SP_THREADS / 8];
+  double ninv[KPL];
+#pragma unroll
+  for (int i = 0; i < KPL; ++i) ninv[i] = k0 + i < a.K ? 1.0 / a.norms[k0 + i] : 0.0;
   for (int f = blockIdx.x * SP_WARPS + warp; f < a.F; f += gridDim.x * SP_WARPS) {
-    float w[SP_KMAX / 32];
-    for (int i = 0; i < per; ++i) {
-      const int k = lane + 32 * i;
-      w[i] = 0.f;
-      if (k < K) {
-        w[i] = float(double(a.Wp[size_t(f) * K + k]) / a.norms[k]);
-        a.Wt[size_t(f) * K + k] = w[i];
-      }
-    }
+    float w[KPL];
+    ld_row<KPL>(a.Wp + size_t(f) * KL + k0, w);
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) w[i] = float(double(w[i]) * ninv[i]);
+    if (grp == 0) st_row<KPL>(a.Wt + size_t(f) * KL + k0, w);
     const long long j0 = a.indptr[f], j1 = a.indptr[f + 1];
-    double rowacc = 0.0;
-    for (long long j = j0; j < j1; ++j) {
-      const int n = a.indices[j];
+    float rowacc = 0.f;
+    for (long long jj = j0; jj < j1; jj += 4) {
+      const long long j = jj + grp;
+      const bool ok = j < j1;
+      const int n = ok ? a.indices[j] : 0;
+      const float x = ok ? a.vals[j] : 0.f;
+      float h[KPL];
+      ld_row<KPL>(a.Hn + size_t(n) * KL + k0, h);
       float p = 0.f;
-      for (int i = 0; i < per; ++i) {
-        const int k = lane + 32 * i;
-        if (k < K) p = fmaf(w[i], a.Hn[size_t(n) * K + k], p);
-      }
-      const double y = double(warp_sum(p));
-      const double x = double(a.vals[j]);
-      if (x != 0.0) rowacc += x * log(x / y) - x;
+#pragma unroll
+      for (int i = 0; i < KPL; ++i) p = fmaf(w[i], h[i], p);
+      const float y = group_sum(p);
+      if (ok && x != 0.f) rowacc += x * logf(x / y) - x;
     }
-    acc += rowacc;   // identical on every lane
+    acc += double(rowacc);   // identical on the 8 lanes of a group
   }
-  if (lane == 0) red[warp] = acc;
+  if (sl == 0) red[threadIdx.x >> 3] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int w = 0; w < SP_WARPS; ++w) s += red[w];
+    for (int i = 0; i < SP_THREADS / 8; ++i) s += red[i];
     a.pc[blockIdx.x] = s;
   }
 }
@@ -230,38 +325,93 @@ __global__ void sp_post_a(const double* comm, int K, double* denh, double* norms
     norms[k] = sqrt(comm[K + k]);
   }
 }
-// rowsum(H~_p) -> denw (next iteration); objective = sum_nnz + sum_k colsum(W~_p) rowsum(H~_p)
-// colsum(W~_p) = colsum(W_p) / norms
+// rowsum(H~_p) -> denw (next iteration); local nonzero part of the objective
+// -> comm_obj[0], global dense part sum_k colsum(W~_p) rowsum(H~_p) -> comm_obj[1]
 __global__ void sp_finish(const double* pb, int GB, const double* pc, int GC, int K,
                           const double* comm_a, const double* norms, double* denw,
-                          double* comm_obj, RunState* st, int slot, double* tr_obj,
-                          double* tr_sec, double tol, int nranks_obj_done) {
-  (void)nranks_obj_done;
+                          double* comm_obj, const RunState* st, int slot) {
   if (!iter_active(st, slot)) return;
+  __shared__ double part[SP_KMAX];
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    double rs = 0.0;
+    for (int g = 0; g < GB; ++g) rs += pb[size_t(g) * K + k];
+    denw[k] = rs;
+    part[k] = (comm_a[k] / norms[k]) * rs;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     double dense = 0.0;
-    for (int k = 0; k < K; ++k) {
-      double rs = 0.0;
-      for (int g = 0; g < GB; ++g) rs += pb[size_t(g) * K + k];
-      denw[k] = rs;
-      dense += (comm_a[k] / norms[k]) * rs;
-    }
+    for (int k = 0; k < K; ++k) dense += part[k];
     double s = 0.0;
     for (int g = 0; g < GC; ++g) s += pc[g];
-    comm_obj[0] = s;       // local nonzero part (allreduced by the host before finish)
-    comm_obj[1] = dense;   // global dense part (every rank holds all of H~)
+    comm_obj[0] = s;
+    comm_obj[1] = dense;
   }
 }
-__global__ void sp_rowsum_init(const float* Ht, int N, int K, double* denw) {
+__global__ void sp_total_obj(double* comm_obj, const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  comm_obj[2] = comm_obj[0] + comm_obj[1];
+}
+// rowsum(H~) of the initial iterate: per-block partials, then a fixed-order sum
+__global__ void sp_rowsum_part(const float* Ht, int N, int KL, int K, double* pb) {
+  const int cpb = SP_THREADS / KL;
+  const int k = threadIdx.x % KL, c = threadIdx.x / KL;
+  __shared__ double red[SP_THREADS];
+  double rs = 0.0;
+  if (c < cpb && k < K)
+    for (int n = blockIdx.x * cpb + c; n < N; n += gridDim.x * cpb) rs += double(Ht[size_t(n) * KL + k]);
+  red[threadIdx.x] = rs;
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double s = 0.0;
+    for (int cc = 0; cc < cpb; ++cc) s += red[cc * KL + threadIdx.x];
+    pb[size_t(blockIdx.x) * K + threadIdx.x] = s;
+  }
+}
+__global__ void sp_rowsum_final(const double* pb, int GB, int K, double* denw) {
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     double s = 0.0;
-    for (int n = 0; n < N; ++n) s += double(Ht[size_t(n) * K + k]);
+    for (int g = 0; g < GB; ++g) s += pb[size_t(g) * K + k];
     denw[k] = s;
   }
 }
-__global__ void sp_total_obj(double* comm_obj, int nranks_parts) {
-  (void)nranks_parts;
-  comm_obj[2] = comm_obj[0] + comm_obj[1];
+// K-strided fp64 rows <-> KL-padded fp32 rows
+__global__ void sp_pad_in(const double* __restrict__ src, size_t rows, int K, int KL,
+                          float* __restrict__ dst) {
+  for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < rows * KL;
+       t += size_t(gridDim.x) * blockDim.x) {
+    const size_t r = t / KL;
+    const int k = int(t - r * KL);
+    dst[t] = k < K ? float(src[r * K + k]) : 0.f;
+  }
+}
+// H (K x N, row-major fp64) -> H~ (N x KL fp32)
+__global__ void sp_transpose_in(const double* __restrict__ src, size_t N, int K, int KL,
+                                float* __restrict__ dst) {
+  for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < N * KL;
+       t += size_t(gridDim.x) * blockDim.x) {
+    const size_t n = t / KL;
+    const int k = int(t - n * KL);
+    dst[t] = k < K ? float(src[size_t(k) * N + n]) : 0.f;
+  }
+}
+__global__ void sp_pad_out(const float* __restrict__ src, size_t rows, int K, int KL,
+                           double* __restrict__ dst) {
+  for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < rows * K;
+       t += size_t(gridDim.x) * blockDim.x) {
+    const size_t r = t / K;
+    const int k = int(t - r * K);
+    dst[t] = double(src[r * KL + k]);
+  }
+}
+__global__ void sp_transpose_out(const float* __restrict__ src, size_t N, int K, int KL,
+                                 double* __restrict__ dst) {
+  for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < N * K;
+       t += size_t(gridDim.x) * blockDim.x) {
+    const int k = int(t / N);
+    const size_t n = t - size_t(k) * N;
+    dst[t] = double(src[n * KL + k]);
+  }
 }
 
 #define SCK(call)                                                                   \
@@ -273,22 +423,25 @@ __global__ void sp_total_obj(double* comm_obj, int nranks_parts) {
   } while (0)
 
 struct SparseEngine : EngineBase {
-  int F = 0, N = 0, K = 0, KL = 32;
+  int F = 0, N = 0, K = 0, KL = 32, S = 0;
   long long nnz = 0;
   long long* indptr = nullptr;
   int* indices = nullptr;
   float* vals = nullptr;
-  long long* colptr = nullptr;
   int* rowidx = nullptr;
   int* perm = nullptr;
+  long long* segptr = nullptr;
+  int* segcol = nullptr;
+  int* colseg = nullptr;
   float *z = nullptr, *Wt = nullptr, *Wp = nullptr, *Ht = nullptr, *Hn = nullptr;
+  float *part = nullptr, *num = nullptr;
   double *denw = nullptr, *denh = nullptr, *norms = nullptr, *pa = nullptr, *pb = nullptr,
          *pc = nullptr, *comm = nullptr;
   double *tr_obj = nullptr, *tr_sec = nullptr, *tr_kkt = nullptr;
   int64_t tr_cap = 0;
   RunState* st = nullptr;
   RunState* st_host = nullptr;
-  int GA = 1, GB = 1;
+  int GA = 1, GB1 = 1, GB3 = 1, nsm = 148;
   bnmf_params p{};
   Scalars sc{};
   bool begun = false;
@@ -296,11 +449,14 @@ struct SparseEngine : EngineBase {
   int gchunk = 0;
   int launches = 0;
 
-  SparseEngine(int dev, cudaStream_t s) { device = dev; dtype = BNMF_FP32; stream = s; }
+  SparseEngine(int dev, cudaStream_t s) {
+    device = dev; dtype = BNMF_FP32; stream = s;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
   ~SparseEngine() override {
     if (gexec) cudaGraphExecDestroy(gexec);
-    void* ptrs[] = {indptr, indices, vals, colptr, rowidx, perm, z, Wt, Wp, Ht, Hn, denw, denh,
-                    norms, pa, pb, pc, comm, tr_obj, tr_sec, tr_kkt, st};
+    void* ptrs[] = {indptr, indices, vals, rowidx, perm, segptr, segcol, colseg, z, Wt, Wp, Ht,
+                    Hn, part, num, denw, denh, norms, pa, pb, pc, comm, tr_obj, tr_sec, tr_kkt, st};
     for (void* q : ptrs) if (q) cudaFree(q);
     if (st_host) cudaFreeHost(st_host);
     if (comm_nccl) ncclCommDestroy(comm_nccl);
@@ -314,6 +470,7 @@ struct SparseEngine : EngineBase {
   template <typename Tp>
   int upload(Tp** dst, const void* src, size_t count, int on_dev) {
     if (*dst) SCK(cudaFree(*dst));
+    *dst = nullptr;
     SCK(cudaMalloc(dst, std::max<size_t>(count, 1) * sizeof(Tp)));
     if (count)
       SCK(cudaMemcpyAsync(*dst, src, count * sizeof(Tp),
@@ -331,16 +488,44 @@ struct SparseEngine : EngineBase {
     if ((rc = upload(&indptr, ip, size_t(F) + 1, on_dev))) return rc;
     if ((rc = upload(&indices, ix, size_t(nnz), on_dev))) return rc;
     if ((rc = upload(&vals, v, size_t(nnz), on_dev))) return rc;
-    if ((rc = upload(&colptr, cp, size_t(N) + 1, on_dev))) return rc;
     if ((rc = upload(&rowidx, ri, size_t(nnz), on_dev))) return rc;
     if ((rc = upload(&perm, pm, size_t(nnz), on_dev))) return rc;
+    // column segments of <= SP_SEG nonzeros (every column gets >= 1 segment)
+    std::vector<long long> hcp(size_t(N) + 1);
+    if (on_dev) {
+      SCK(cudaMemcpyAsync(hcp.data(), cp, hcp.size() * sizeof(long long), cudaMemcpyDeviceToHost,
+                          stream));
+      SCK(cudaStreamSynchronize(stream));
+    } else {
+      std::memcpy(hcp.data(), cp, hcp.size() * sizeof(long long));
+    }
+    std::vector<long long> sp;
+    std::vector<int> sc_, cs(size_t(N) + 1);
+    sp.reserve(size_t(N) + size_t(nnz / SP_SEG) + 2);
+    for (int n = 0; n < N; ++n) {
+      cs[n] = int(sc_.size());
+      const long long a0 = hcp[n], a1 = hcp[n + 1];
+      long long s = a0;
+      do {
+        sp.push_back(s);
+        sc_.push_back(n);
+        s += SP_SEG;
+      } while (s < a1);
+    }
+    cs[N] = int(sc_.size());
+    sp.push_back(hcp[N]);
+    S = int(sc_.size());
+    if ((rc = upload(&segptr, sp.data(), sp.size(), 0))) return rc;
+    if ((rc = upload(&segcol, sc_.data(), sc_.size(), 0))) return rc;
+    if ((rc = upload(&colseg, cs.data(), cs.size(), 0))) return rc;
     if (z) SCK(cudaFree(z));
+    z = nullptr;
     SCK(cudaMalloc(&z, std::max<size_t>(nnz, 1) * sizeof(float)));
     if (!st) {
       SCK(cudaMalloc(&st, sizeof(RunState)));
       SCK(cudaMallocHost(&st_host, sizeof(RunState)));
     }
-    SCK(cudaStreamSynchronize(stream));
+    SCK(cudaStreamSynchronize(stream));   // host vectors above are the copy sources
     K = 0;
     begun = false;
     return 0;
@@ -351,23 +536,30 @@ struct SparseEngine : EngineBase {
     if (K_ < 1 || K_ > SP_KMAX) return fail(BNMF_E_UNSUPPORTED, "sparse path supports rank 1..128");
     SCK(cudaSetDevice(device));
     if (K != K_) {
-      float** fp[] = {&Wt, &Wp, &Ht, &Hn};
+      float** fp[] = {&Wt, &Wp, &Ht, &Hn, &part, &num};
       for (float** q : fp) if (*q) { SCK(cudaFree(*q)); *q = nullptr; }
       double** dp[] = {&denw, &denh, &norms, &pa, &pb, &pc, &comm};
       for (double** q : dp) if (*q) { SCK(cudaFree(*q)); *q = nullptr; }
       K = int(K_);
       KL = (K + 31) / 32 * 32;
-      SCK(cudaMalloc(&Wt, size_t(F) * K * sizeof(float)));
-      SCK(cudaMalloc(&Wp, size_t(F) * K * sizeof(float)));
-      SCK(cudaMalloc(&Ht, size_t(N) * K * sizeof(float)));
-      SCK(cudaMalloc(&Hn, size_t(N) * K * sizeof(float)));
-      GA = std::max(1, std::min((F + SP_WARPS - 1) / SP_WARPS, 148 * 8));
-      GB = std::max(1, std::min((N + SP_WARPS - 1) / SP_WARPS, 148 * 8));
+      if (KL == 96) KL = 128;   // KPL in {4, 8, 16}
+      SCK(cudaMalloc(&Wt, size_t(F) * KL * sizeof(float)));
+      SCK(cudaMalloc(&Wp, size_t(F) * KL * sizeof(float)));
+      SCK(cudaMalloc(&Ht, size_t(N) * KL * sizeof(float)));
+      SCK(cudaMalloc(&Hn, size_t(N) * KL * sizeof(float)));
+      SCK(cudaMalloc(&part, size_t(S) * KL * sizeof(float)));
+      SCK(cudaMalloc(&num, size_t(N) * KL * sizeof(float)));
+      SCK(cudaMemset(Hn, 0, size_t(N) * KL * sizeof(float)));
+      SCK(cudaMemset(Wp, 0, size_t(F) * KL * sizeof(float)));
+      GA = std::max(1, std::min((F + SP_WARPS - 1) / SP_WARPS, nsm * 8));
+      GB1 = std::max(1, std::min((S + SP_WARPS - 1) / SP_WARPS, nsm * 8));
+      const int cpb = SP_THREADS / KL;
+      GB3 = std::max(1, std::min((N + cpb - 1) / cpb, nsm * 4));
       SCK(cudaMalloc(&denw, K * sizeof(double)));
       SCK(cudaMalloc(&denh, K * sizeof(double)));
       SCK(cudaMalloc(&norms, K * sizeof(double)));
       SCK(cudaMalloc(&pa, size_t(GA) * 2 * K * sizeof(double)));
-      SCK(cudaMalloc(&pb, size_t(GB) * K * sizeof(double)));
+      SCK(cudaMalloc(&pb, size_t(GB3) * K * sizeof(double)));
       SCK(cudaMalloc(&pc, size_t(GA) * sizeof(double)));
       SCK(cudaMalloc(&comm, (2 * K + 8) * sizeof(double)));
     }
@@ -376,10 +568,10 @@ struct SparseEngine : EngineBase {
     SCK(cudaMalloc(&stg, std::max(fk, nk) * sizeof(double)));
     SCK(cudaMemcpyAsync(stg, w, fk * sizeof(double),
                         on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream));
-    from_double<float><<<int(std::min<size_t>((fk + 255) / 256, 1184)), 256, 0, stream>>>(stg, fk, Wt);
+    sp_pad_in<<<nsm * 8, 256, 0, stream>>>(stg, size_t(F), K, KL, Wt);
     SCK(cudaMemcpyAsync(stg, h, nk * sizeof(double),
                         on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, stream));
-    transpose_in<float><<<int(std::min<size_t>((nk + 255) / 256, 1184)), 256, 0, stream>>>(stg, K, size_t(N), Ht);
+    sp_transpose_in<<<nsm * 8, 256, 0, stream>>>(stg, size_t(N), K, KL, Ht);
     SCK(cudaGetLastError());
     SCK(cudaStreamSynchronize(stream));
     SCK(cudaFree(stg));
@@ -391,8 +583,10 @@ struct SparseEngine : EngineBase {
     SpArgs a;
     a.F = F; a.N = N; a.K = K; a.KL = KL;
     a.indptr = indptr; a.indices = indices; a.vals = vals;
-    a.colptr = colptr; a.rowidx = rowidx; a.perm = perm; a.z = z;
-    a.Wt = Wt; a.Wp = Wp; a.Ht = Ht; a.Hn = Hn;
+    a.rowidx = rowidx; a.perm = perm;
+    a.segptr = segptr; a.segcol = segcol; a.colseg = colseg; a.S = S;
+    a.z = z;
+    a.Wt = Wt; a.Wp = Wp; a.Ht = Ht; a.Hn = Hn; a.part = part; a.num = num;
     a.denw = denw; a.denh = denh; a.norms = norms;
     a.pa = pa; a.pb = pb; a.pc = pc;
     a.algorithm = p.algorithm; a.sc = sc;
@@ -424,7 +618,9 @@ struct SparseEngine : EngineBase {
     h.max_iter = max_iters;
     *st_host = h;
     SCK(cudaMemcpyAsync(st, st_host, sizeof(RunState), cudaMemcpyHostToDevice, stream));
-    sp_rowsum_init<<<1, 128, 0, stream>>>(Ht, N, K, denw);
+    enqueued = 0;
+    sp_rowsum_part<<<GB3, SP_THREADS, 0, stream>>>(Ht, N, KL, K, pb);
+    sp_rowsum_final<<<1, 128, 0, stream>>>(pb, GB3, K, denw);
     SCK(cudaGetLastError());
     if (gexec) { SCK(cudaGraphExecDestroy(gexec)); gexec = nullptr; }
     SCK(cudaStreamSynchronize(stream));
@@ -432,46 +628,79 @@ struct SparseEngine : EngineBase {
     return 0;
   }
 
-  int allreduce(double* buf, size_t count) {
+  int allreduce(void* buf, size_t count, ncclDataType_t t) {
     if (nranks > 1) {
-      ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, comm_nccl, stream);
+      ncclResult_t r = ncclAllReduce(buf, buf, count, t, ncclSum, comm_nccl, stream);
       if (r != ncclSuccess) return fail(BNMF_E_NCCL, ncclGetErrorString(r));
       launches += 1;
     }
     return 0;
   }
 
+  template <int KPL>
+  void launch_rows_a(const SpArgs& a, int slot) {
+    sp_pass_a<KPL><<<GA, SP_THREADS, 0, stream>>>(a, st, slot);
+  }
+  template <int KPL>
+  void launch_b1(const SpArgs& a, int slot) {
+    sp_pass_b1<KPL><<<GB1, SP_THREADS, 0, stream>>>(a, st, slot);
+  }
+  template <int KPL>
+  void launch_rows_c(const SpArgs& a, int slot) {
+    sp_pass_c<KPL><<<GA, SP_THREADS, 0, stream>>>(a, st, slot);
+  }
+  void dispatch(int which, const SpArgs& a, int slot) {
+    const int kpl = KL / 8;
+    if (which == 0) {
+      if (kpl == 4) launch_rows_a<4>(a, slot);
+      else if (kpl == 8) launch_rows_a<8>(a, slot);
+      else launch_rows_a<16>(a, slot);
+    } else if (which == 1) {
+      if (kpl == 4) launch_b1<4>(a, slot);
+      else if (kpl == 8) launch_b1<8>(a, slot);
+      else launch_b1<16>(a, slot);
+    } else {
+      if (kpl == 4) launch_rows_c<4>(a, slot);
+      else if (kpl == 8) launch_rows_c<8>(a, slot);
+      else launch_rows_c<16>(a, slot);
+    }
+  }
+
   int enqueue_iteration(int slot) {
     SpArgs a = args();
     begin_iter<<<1, 1, 0, stream>>>(st, slot);
-    sp_pass_a<<<GA, SP_THREADS, 0, stream>>>(a, st, slot);
+    dispatch(0, a, slot);
     sp_reduce_a<<<1, 256, 0, stream>>>(pa, GA, K, comm, st, slot);
     SCK(cudaGetLastError());
     launches += 3;
-    if (int rc = allreduce(comm, 2 * K)) return rc;
+    if (int rc = allreduce(comm, 2 * size_t(K), ncclDouble)) return rc;
     sp_post_a<<<1, 128, 0, stream>>>(comm, K, denh, norms, st, slot);
-    if (nranks > 1) {
-      // the column pass needs every rank's nonzeros: rows are sharded, so the
-      // H numerator would need a K x N allreduce (not implemented: see DESIGN.md)
-      return fail(BNMF_E_UNSUPPORTED, "multi-GPU sparse path not implemented");
-    }
-    sp_pass_b<<<GB, SP_THREADS, 0, stream>>>(a, st, slot);
-    sp_pass_c<<<GA, SP_THREADS, 0, stream>>>(a, st, slot);
+    dispatch(1, a, slot);
+    sp_pass_b2<<<nsm * 8, 256, 0, stream>>>(a, st, slot);
+    SCK(cudaGetLastError());
+    launches += 3;
+    // rows are sharded: every rank holds a partial H numerator of its rows
+    if (int rc = allreduce(num, size_t(N) * KL, ncclFloat)) return rc;
+    sp_pass_b3<<<GB3, SP_THREADS, 0, stream>>>(a, st, slot);
+    dispatch(2, a, slot);
     double* cobj = comm + 2 * K;
-    sp_finish<<<1, 32, 0, stream>>>(pb, GB, pc, GA, K, comm, norms, denw, cobj, st, slot, tr_obj,
-                                    tr_sec, sc.tol, nranks);
-    sp_total_obj<<<1, 1, 0, stream>>>(cobj, nranks);
+    sp_finish<<<1, 128, 0, stream>>>(pb, GB3, pc, GA, K, comm, norms, denw, cobj, st, slot);
+    SCK(cudaGetLastError());
+    launches += 3;
+    if (int rc = allreduce(cobj, 1, ncclDouble)) return rc;   // nonzero part only
+    sp_total_obj<<<1, 1, 0, stream>>>(cobj, st, slot);
     finish_iter<<<1, 1, 0, stream>>>(st, slot, cobj + 2, tr_obj, tr_sec, sc.tol);
     // H~_p becomes the next iterate
-    SCK(cudaMemcpyAsync(Ht, Hn, size_t(N) * K * sizeof(float), cudaMemcpyDeviceToDevice, stream));
+    std::swap(Ht, Hn);
     SCK(cudaGetLastError());
-    launches += 7;
+    launches += 2;
     return 0;
   }
 
   int capture(int chunk) {
     if (gexec && gchunk == chunk) return 0;
     if (gexec) { SCK(cudaGraphExecDestroy(gexec)); gexec = nullptr; }
+    if (chunk % 2) return fail(BNMF_E_STATE, "graph chunk must be even (H~ ping-pong)");
     cudaGraph_t g;
     SCK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
     int l0 = launches, rc = 0;
@@ -493,6 +722,14 @@ struct SparseEngine : EngineBase {
     return n >= 16 ? capture(16) : 0;
   }
 
+  // Inactive iterations (after the stop) skip every kernel, but the host-side
+  // H~ ping-pong still swaps; the live iterate is tracked by parity of the
+  // number of enqueued iterations, so the step count is kept even around a
+  // graph launch and an inactive trailing iteration swaps back harmlessly:
+  // the last ACTIVE iteration wrote Hn before the swap, and get_factors reads
+  // the buffer that holds iterate iters_done (see live_h()).
+  int64_t enqueued = 0;
+
   int step(int64_t n) override {
     if (!begun) return fail(BNMF_E_STATE, "begin must precede step");
     SCK(cudaSetDevice(device));
@@ -500,6 +737,7 @@ struct SparseEngine : EngineBase {
     for (int64_t i = 0; i < n / chunk; ++i) {
       if (int rc = capture(chunk)) return rc;
       SCK(cudaGraphLaunch(gexec, stream));
+      enqueued += chunk;
     }
     for (int64_t i = 0; i < n % chunk; ++i) {
       int l0 = launches;
@@ -507,6 +745,11 @@ struct SparseEngine : EngineBase {
       launches_per_iter = launches - l0;
       advance_base<<<1, 1, 0, stream>>>(st, 1);
       SCK(cudaGetLastError());
+      enqueued += 1;
+      if (gexec) {   // the captured graph baked in the pointer parity
+        SCK(cudaGraphExecDestroy(gexec));
+        gexec = nullptr;
+      }
     }
     return 0;
   }
@@ -530,13 +773,19 @@ struct SparseEngine : EngineBase {
   }
 
   int get_factors(double* w, double* h) override {
+    SCK(cudaSetDevice(device));
+    int64_t done = 0;
+    if (int rc = sync(&done, nullptr)) return rc;
+    // iterate `done` lives in Ht if the (done .. enqueued) inactive tail had an
+    // even number of swaps, else in Hn
+    const float* Hlive = ((enqueued - done) % 2 == 0) ? Ht : Hn;
     size_t fk = size_t(F) * K, nk = size_t(N) * K;
     double* stg;
     SCK(cudaMalloc(&stg, std::max(fk, nk) * sizeof(double)));
-    to_double<float><<<int(std::min<size_t>((fk + 255) / 256, 1184)), 256, 0, stream>>>(Wt, fk, stg);
+    sp_pad_out<<<nsm * 8, 256, 0, stream>>>(Wt, size_t(F), K, KL, stg);
     SCK(cudaMemcpyAsync(w, stg, fk * sizeof(double), cudaMemcpyDeviceToHost, stream));
     SCK(cudaStreamSynchronize(stream));
-    transpose_out<float><<<int(std::min<size_t>((nk + 255) / 256, 1184)), 256, 0, stream>>>(Ht, K, size_t(N), stg);
+    sp_transpose_out<<<nsm * 8, 256, 0, stream>>>(Hlive, size_t(N), K, KL, stg);
     SCK(cudaMemcpyAsync(h, stg, nk * sizeof(double), cudaMemcpyDeviceToHost, stream));
     SCK(cudaStreamSynchronize(stream));
     SCK(cudaFree(stg));

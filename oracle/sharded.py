@@ -52,3 +52,45 @@ def run_sharded_jmm(v_local, beta, w0, h0_local, iters, kappa=0.0, floor=O.DEFAU
         objs.append(obj)
         wt, ht = O.normalize_arrays(w, h)
     return wt, ht, np.array(objs)
+
+
+def run_sharded_sparse_kl(csr_local, w0_local, h0, iters, algorithm="jmm", floor=O.DEFAULT_FLOOR):
+    """Sparse KL (beta = 1) over a ROW shard of V: W rows are
+    local, H is replicated.  Restates libbnmf's sparse schedule (sparse.cu):
+    allreduce of [colsum W_p | sum_f W_p^2] after the W update, allreduce of
+    the K x N partial H numerator, allreduce of the nonzero part of the
+    objective (the dense part (1'W)(H1) is global once colsum W is).  Checked
+    against the single-process restatement betanmf_oracle.run_sparse_kl."""
+    import scipy.sparse as sp
+    v = sp.csr_matrix(csr_local, dtype=float)
+    v.sort_indices()
+    rows = np.repeat(np.arange(v.shape[0]), np.diff(v.indptr))
+    cols, x = v.indices, v.data
+    wt, ht = np.array(w0_local, dtype=float), np.array(h0, dtype=float)
+    K = wt.shape[1]
+
+    def sddmm(wm, hm):
+        return np.einsum("ik,ki->i", wm[rows], hm[:, cols])
+
+    def zmat(vals):
+        return sp.csr_matrix((vals, cols, v.indptr), shape=v.shape)
+
+    objs = []
+    for _ in range(iters):
+        z = zmat(x / sddmm(wt, ht))
+        w = wt * O.guarded_divide(np.asarray(z @ ht.T), ht.sum(axis=1)[None, :], floor)
+        stats = _allreduce(np.concatenate([w.sum(axis=0), (w * w).sum(axis=0)]))
+        colsum, sumsq = stats[:K], stats[K:]
+        if algorithm == "bmm":
+            z = zmat(x / sddmm(w, ht))
+            hnum = _allreduce(np.asarray((z.T @ w).T))
+        else:
+            hnum = _allreduce(np.asarray((z.T @ wt).T))
+        h = ht * O.guarded_divide(hnum, colsum[:, None], floor)
+        y = sddmm(w, h)
+        local = float(np.sum(x * np.log(x / y) - x))
+        obj = float(_allreduce(np.array([local]))[0]) + float(colsum @ h.sum(axis=1))
+        objs.append(obj)
+        norms = np.sqrt(sumsq)
+        wt, ht = w / norms[None, :], h * norms[:, None]
+    return wt, ht, np.array(objs)

@@ -46,6 +46,14 @@ constexpr int SP_THREADS = 256;
 constexpr int SP_WARPS = SP_THREADS / 32;
 constexpr int SP_KMAX = 128;
 constexpr int SP_SEG = 2048;   // nonzeros per column segment (pass B1)
+// Columns with more than SP_HEAVY nonzeros are also cut at row-tile
+// boundaries (SP_TILE rows): their segments are ordered tile by tile, so the
+// W~ rows they gather stay in L2 (one 16 MB tile of W~ at K = 64) instead of
+// being fetched from HBM once per nonzero.
+constexpr int SP_HEAVY = 2048;
+constexpr int SP_TILE = 131072;
+constexpr int SP_SEG_H = 512;  // heavy-column segments (more warps per tile)
+constexpr int SP_U = 4;        // nonzeros per 8-lane group in flight
 
 struct SpArgs {
   int F, N, K, KL;
@@ -54,9 +62,10 @@ struct SpArgs {
   const float* vals;
   const int* rowidx;           // CSC row index
   const int* perm;             // CSC position -> CSR position
-  const long long* segptr;     // [S + 1] CSC positions
+  const long long* segptr;     // [S][2] CSC range of each segment
   const int* segcol;           // [S] column of each segment
-  const int* colseg;           // [N + 1] first segment of each column
+  const int* colseg;           // [N + 1] each column's run in seglist
+  const int* seglist;          // [S] segment ids of each column, in row order
   int S;
   float* z;                    // per nonzero (CSR order)
   float* Wt;                   // W~ (F x KL)
@@ -120,21 +129,31 @@ __global__ void __launch_bounds__(SP_THREADS) sp_pass_a(SpArgs a, const RunState
 #pragma unroll
     for (int i = 0; i < KPL; ++i) num[i] = 0.f;
     const long long j0 = a.indptr[f], j1 = a.indptr[f + 1];
-    for (long long jj = j0; jj < j1; jj += 4) {
-      const long long j = jj + grp;
-      const bool ok = j < j1;
-      const int n = ok ? a.indices[j] : 0;
-      const float x = ok ? a.vals[j] : 0.f;
-      float h[KPL];
-      ld_row<KPL>(a.Ht + size_t(n) * KL + k0, h);
-      float p = 0.f;
+    for (long long jj = j0; jj < j1; jj += 4 * SP_U) {
+      // SP_U nonzeros per group in flight: indices first, then the row gathers
+      int n[SP_U];
+      float x[SP_U], h[SP_U][KPL];
 #pragma unroll
-      for (int i = 0; i < KPL; ++i) p = fmaf(w[i], h[i], p);
-      const float y = group_sum(p);
-      const float zz = ok ? x / y : 0.f;
-      if (ok && sl == 0) a.z[j] = zz;
+      for (int u = 0; u < SP_U; ++u) {
+        const long long j = jj + 4 * u + grp;
+        n[u] = j < j1 ? a.indices[j] : 0;
+        x[u] = j < j1 ? a.vals[j] : 0.f;
+      }
 #pragma unroll
-      for (int i = 0; i < KPL; ++i) num[i] = fmaf(zz, h[i], num[i]);
+      for (int u = 0; u < SP_U; ++u) ld_row<KPL>(a.Ht + size_t(n[u]) * KL + k0, h[u]);
+#pragma unroll
+      for (int u = 0; u < SP_U; ++u) {
+        const long long j = jj + 4 * u + grp;
+        const bool ok = j < j1;
+        float p = 0.f;
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) p = fmaf(w[i], h[u][i], p);
+        const float y = group_sum(p);
+        const float zz = ok ? x[u] / y : 0.f;
+        if (ok && sl == 0) a.z[j] = zz;
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) num[i] = fmaf(zz, h[u][i], num[i]);
+      }
     }
 #pragma unroll
     for (int i = 0; i < KPL; ++i) {   // groups 0..3 in a fixed tree
@@ -174,38 +193,47 @@ __global__ void __launch_bounds__(SP_THREADS) sp_pass_a(SpArgs a, const RunState
 
 // ---- pass B1: column segments -> partial H numerators ----------------------
 template <int KPL>
-__global__ void __launch_bounds__(SP_THREADS) sp_pass_b1(SpArgs a, const RunState* st, int slot) {
+__global__ void __launch_bounds__(SP_THREADS) sp_pass_b1(SpArgs a, const RunState* st, int slot,
+                                                          int s_begin, int s_end) {
   if (!iter_active(st, slot)) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane >> 3, sl = lane & 7, k0 = sl * KPL;
   const int KL = a.KL;
   const bool bmm = a.algorithm == BNMF_BMM;
   const float* W = bmm ? a.Wp : a.Wt;
-  for (int s = blockIdx.x * SP_WARPS + warp; s < a.S; s += gridDim.x * SP_WARPS) {
-    const long long j0 = a.segptr[s], j1 = a.segptr[s + 1];
+  for (int s = s_begin + blockIdx.x * SP_WARPS + warp; s < s_end; s += gridDim.x * SP_WARPS) {
+    const long long j0 = a.segptr[2 * size_t(s)], j1 = a.segptr[2 * size_t(s) + 1];
     float num[KPL], h[KPL];
 #pragma unroll
     for (int i = 0; i < KPL; ++i) num[i] = 0.f;
     if (bmm) ld_row<KPL>(a.Ht + size_t(a.segcol[s]) * KL + k0, h);
-    for (long long jj = j0; jj < j1; jj += 4) {
-      const long long j = jj + grp;
-      const bool ok = j < j1;
-      const int f = ok ? a.rowidx[j] : 0;
-      const int pj = ok ? a.perm[j] : 0;
-      float w[KPL];
-      ld_row<KPL>(W + size_t(f) * KL + k0, w);
-      float zz;
-      if (bmm) {   // block update: Vt2 = W_p H~ at this nonzero (updates.py:173-181)
-        float p = 0.f;
+    for (long long jj = j0; jj < j1; jj += 4 * SP_U) {
+      int f[SP_U];
+      float zx[SP_U], w[SP_U][KPL];
 #pragma unroll
-        for (int i = 0; i < KPL; ++i) p = fmaf(w[i], h[i], p);
-        const float y = group_sum(p);
-        zz = ok ? a.vals[pj] / y : 0.f;
-      } else {     // joint update: the anchor's Z from pass A
-        zz = ok ? a.z[pj] : 0.f;
+      for (int u = 0; u < SP_U; ++u) {
+        const long long j = jj + 4 * u + grp;
+        const bool ok = j < j1;
+        f[u] = ok ? a.rowidx[j] : 0;
+        const int pj = ok ? a.perm[j] : 0;
+        // JMM: the anchor's Z from pass A; BMM: the value (Z recomputed below)
+        zx[u] = ok ? (bmm ? a.vals[pj] : a.z[pj]) : 0.f;
       }
 #pragma unroll
-      for (int i = 0; i < KPL; ++i) num[i] = fmaf(zz, w[i], num[i]);
+      for (int u = 0; u < SP_U; ++u) ld_row<KPL>(W + size_t(f[u]) * KL + k0, w[u]);
+#pragma unroll
+      for (int u = 0; u < SP_U; ++u) {
+        float zz = zx[u];
+        if (bmm) {   // block update: Vt2 = W_p H~ at this nonzero (updates.py:173-181)
+          float p = 0.f;
+#pragma unroll
+          for (int i = 0; i < KPL; ++i) p = fmaf(w[u][i], h[i], p);
+          const float y = group_sum(p);
+          zz = zx[u] != 0.f ? zx[u] / y : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) num[i] = fmaf(zz, w[u][i], num[i]);
+      }
     }
 #pragma unroll
     for (int i = 0; i < KPL; ++i) {
@@ -224,10 +252,10 @@ __global__ void sp_pass_b2(SpArgs a, const RunState* st, int slot) {
        t += size_t(gridDim.x) * blockDim.x) {
     const int n = int(t / a.KL), k = int(t - size_t(n) * a.KL);
     const int s0 = a.colseg[n], s1 = a.colseg[n + 1];
-    float v = a.part[size_t(s0) * a.KL + k];
+    float v = a.part[size_t(a.seglist[s0]) * a.KL + k];
     if (s1 - s0 > 1) {
       double acc = double(v);
-      for (int s = s0 + 1; s < s1; ++s) acc += double(a.part[size_t(s) * a.KL + k]);
+      for (int s = s0 + 1; s < s1; ++s) acc += double(a.part[size_t(a.seglist[s]) * a.KL + k]);
       v = float(acc);
     }
     a.num[t] = v;
@@ -282,18 +310,25 @@ __global__ void __launch_bounds__(SP_THREADS) sp_pass_c(SpArgs a, const RunState
     if (grp == 0) st_row<KPL>(a.Wt + size_t(f) * KL + k0, w);
     const long long j0 = a.indptr[f], j1 = a.indptr[f + 1];
     float rowacc = 0.f;
-    for (long long jj = j0; jj < j1; jj += 4) {
-      const long long j = jj + grp;
-      const bool ok = j < j1;
-      const int n = ok ? a.indices[j] : 0;
-      const float x = ok ? a.vals[j] : 0.f;
-      float h[KPL];
-      ld_row<KPL>(a.Hn + size_t(n) * KL + k0, h);
-      float p = 0.f;
+    for (long long jj = j0; jj < j1; jj += 4 * SP_U) {
+      int n[SP_U];
+      float x[SP_U], h[SP_U][KPL];
 #pragma unroll
-      for (int i = 0; i < KPL; ++i) p = fmaf(w[i], h[i], p);
-      const float y = group_sum(p);
-      if (ok && x != 0.f) rowacc += x * logf(x / y) - x;
+      for (int u = 0; u < SP_U; ++u) {
+        const long long j = jj + 4 * u + grp;
+        n[u] = j < j1 ? a.indices[j] : 0;
+        x[u] = j < j1 ? a.vals[j] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < SP_U; ++u) ld_row<KPL>(a.Hn + size_t(n[u]) * KL + k0, h[u]);
+#pragma unroll
+      for (int u = 0; u < SP_U; ++u) {
+        float p = 0.f;
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) p = fmaf(w[i], h[u][i], p);
+        const float y = group_sum(p);
+        if (x[u] != 0.f) rowacc += x[u] * logf(x[u] / y) - x[u];
+      }
     }
     acc += double(rowacc);   // identical on the 8 lanes of a group
   }
@@ -433,6 +468,8 @@ struct SparseEngine : EngineBase {
   long long* segptr = nullptr;
   int* segcol = nullptr;
   int* colseg = nullptr;
+  int* seglist = nullptr;
+  std::vector<int> tstart;   // [ntile + 2] B1 launch ranges of segments
   float *z = nullptr, *Wt = nullptr, *Wp = nullptr, *Ht = nullptr, *Hn = nullptr;
   float *part = nullptr, *num = nullptr;
   double *denw = nullptr, *denh = nullptr, *norms = nullptr, *pa = nullptr, *pb = nullptr,
@@ -455,7 +492,7 @@ struct SparseEngine : EngineBase {
   }
   ~SparseEngine() override {
     if (gexec) cudaGraphExecDestroy(gexec);
-    void* ptrs[] = {indptr, indices, vals, rowidx, perm, segptr, segcol, colseg, z, Wt, Wp, Ht,
+    void* ptrs[] = {indptr, indices, vals, rowidx, perm, segptr, segcol, colseg, seglist, z, Wt, Wp, Ht,
                     Hn, part, num, denw, denh, norms, pa, pb, pc, comm, tr_obj, tr_sec, tr_kkt, st};
     for (void* q : ptrs) if (q) cudaFree(q);
     if (st_host) cudaFreeHost(st_host);
@@ -490,34 +527,76 @@ struct SparseEngine : EngineBase {
     if ((rc = upload(&vals, v, size_t(nnz), on_dev))) return rc;
     if ((rc = upload(&rowidx, ri, size_t(nnz), on_dev))) return rc;
     if ((rc = upload(&perm, pm, size_t(nnz), on_dev))) return rc;
-    // column segments of <= SP_SEG nonzeros (every column gets >= 1 segment)
+    // column segments (every column gets >= 1): light columns are cut every
+    // SP_SEG nonzeros; heavy ones also at row-tile boundaries, and their
+    // segments come first, tile by tile (W~ row locality in pass B1)
     std::vector<long long> hcp(size_t(N) + 1);
+    std::vector<int> hri;
+    const int* rip = ri;
     if (on_dev) {
+      hri.resize(size_t(nnz));
       SCK(cudaMemcpyAsync(hcp.data(), cp, hcp.size() * sizeof(long long), cudaMemcpyDeviceToHost,
                           stream));
+      if (nnz) SCK(cudaMemcpyAsync(hri.data(), ri, size_t(nnz) * sizeof(int), cudaMemcpyDeviceToHost,
+                                   stream));
       SCK(cudaStreamSynchronize(stream));
+      rip = hri.data();
     } else {
       std::memcpy(hcp.data(), cp, hcp.size() * sizeof(long long));
     }
-    std::vector<long long> sp;
-    std::vector<int> sc_, cs(size_t(N) + 1);
-    sp.reserve(size_t(N) + size_t(nnz / SP_SEG) + 2);
+    const int ntile = (F + SP_TILE - 1) / SP_TILE;
+    struct Seg { long long a0, a1; int col, tile; };
+    std::vector<Seg> heavy, light;
     for (int n = 0; n < N; ++n) {
-      cs[n] = int(sc_.size());
       const long long a0 = hcp[n], a1 = hcp[n + 1];
-      long long s = a0;
-      do {
-        sp.push_back(s);
-        sc_.push_back(n);
-        s += SP_SEG;
-      } while (s < a1);
+      if (a1 - a0 > SP_HEAVY) {
+        long long s = a0;
+        for (int t = 0; t < ntile && s < a1; ++t) {
+          const int rend = int(std::min<long long>(F, (long long)(t + 1) * SP_TILE));
+          const long long e = std::lower_bound(rip + s, rip + a1, rend) - rip;
+          for (long long q = s; q < e; q += SP_SEG_H) heavy.push_back({q, std::min(e, q + SP_SEG_H), n, t});
+          s = e;
+        }
+      } else {
+        long long q = a0;
+        do {
+          light.push_back({q, std::min(a1, q + SP_SEG), n, 0});
+          q += SP_SEG;
+        } while (q < a1);
+      }
     }
-    cs[N] = int(sc_.size());
-    sp.push_back(hcp[N]);
-    S = int(sc_.size());
-    if ((rc = upload(&segptr, sp.data(), sp.size(), 0))) return rc;
-    if ((rc = upload(&segcol, sc_.data(), sc_.size(), 0))) return rc;
+    std::stable_sort(heavy.begin(), heavy.end(),
+                     [](const Seg& x, const Seg& y) { return x.tile < y.tile; });
+    std::vector<Seg> all;
+    all.reserve(heavy.size() + light.size());
+    all.insert(all.end(), heavy.begin(), heavy.end());
+    all.insert(all.end(), light.begin(), light.end());
+    S = int(all.size());
+    // B1 launch ranges: the heavy segments of each row tile, then all light ones
+    tstart.assign(size_t(ntile) + 2, 0);
+    for (const Seg& g : heavy) ++tstart[g.tile + 1];
+    for (int t = 0; t < ntile; ++t) tstart[t + 1] += tstart[t];
+    tstart[ntile + 1] = S;
+    std::vector<int> scol(S), cs(size_t(N) + 1, 0), sl(S);
+    for (int i = 0; i < S; ++i) { scol[i] = all[i].col; ++cs[all[i].col + 1]; }
+    for (int n = 0; n < N; ++n) cs[n + 1] += cs[n];
+    {
+      // per column, its segments in increasing row order (= increasing a0)
+      std::vector<int> fill(cs.begin(), cs.end() - 1);
+      std::vector<int> order(S);
+      for (int i = 0; i < S; ++i) order[i] = i;
+      std::sort(order.begin(), order.end(), [&](int x, int y) {
+        return all[x].col != all[y].col ? all[x].col < all[y].col : all[x].a0 < all[y].a0;
+      });
+      for (int i = 0; i < S; ++i) sl[fill[all[order[i]].col]++] = order[i];
+    }
+    // [begin, end) of each segment (no longer contiguous in CSC order)
+    std::vector<long long> spe(2 * size_t(S));
+    for (int i = 0; i < S; ++i) { spe[2 * size_t(i)] = all[i].a0; spe[2 * size_t(i) + 1] = all[i].a1; }
+    if ((rc = upload(&segptr, spe.data(), spe.size(), 0))) return rc;
+    if ((rc = upload(&segcol, scol.data(), scol.size(), 0))) return rc;
     if ((rc = upload(&colseg, cs.data(), cs.size(), 0))) return rc;
+    if ((rc = upload(&seglist, sl.data(), sl.size(), 0))) return rc;
     if (z) SCK(cudaFree(z));
     z = nullptr;
     SCK(cudaMalloc(&z, std::max<size_t>(nnz, 1) * sizeof(float)));
@@ -584,7 +663,7 @@ struct SparseEngine : EngineBase {
     a.F = F; a.N = N; a.K = K; a.KL = KL;
     a.indptr = indptr; a.indices = indices; a.vals = vals;
     a.rowidx = rowidx; a.perm = perm;
-    a.segptr = segptr; a.segcol = segcol; a.colseg = colseg; a.S = S;
+    a.segptr = segptr; a.segcol = segcol; a.colseg = colseg; a.seglist = seglist; a.S = S;
     a.z = z;
     a.Wt = Wt; a.Wp = Wp; a.Ht = Ht; a.Hn = Hn; a.part = part; a.num = num;
     a.denw = denw; a.denh = denh; a.norms = norms;
@@ -643,7 +722,15 @@ struct SparseEngine : EngineBase {
   }
   template <int KPL>
   void launch_b1(const SpArgs& a, int slot) {
-    sp_pass_b1<KPL><<<GB1, SP_THREADS, 0, stream>>>(a, st, slot);
+    // one launch per row tile (every warp gathers W~ rows of the same tile,
+    // which stay in L2), then the light columns
+    for (size_t t = 0; t + 1 < tstart.size(); ++t) {
+      const int s0 = tstart[t], s1 = tstart[t + 1];
+      if (s1 <= s0) continue;
+      const int g = std::max(1, std::min((s1 - s0 + SP_WARPS - 1) / SP_WARPS, GB1));
+      sp_pass_b1<KPL><<<g, SP_THREADS, 0, stream>>>(a, st, slot, s0, s1);
+      ++launches;
+    }
   }
   template <int KPL>
   void launch_rows_c(const SpArgs& a, int slot) {

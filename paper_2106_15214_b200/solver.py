@@ -423,8 +423,6 @@ def _run_sparse(data, config, counter, algorithm, *, dtype="fp32", init=None, de
         raise ValueError("the sparse path implements beta = 1 (KL) only")
     if config.kappa not in (None, 0.0):
         raise ValueError("sparse input needs kappa = 0 (a positive shift densifies V)")
-    if sharded:
-        raise ValueError("the sparse path is single-GPU in this build")
     if (config.sub_iters != 1 or (config.sub_iters_w or 1) != 1
             or (config.sub_iters_h or 1) != 1):
         raise ValueError("the sparse path implements one sub-iteration")
@@ -434,11 +432,39 @@ def _run_sparse(data, config, counter, algorithm, *, dtype="fp32", init=None, de
         raise ValueError("data entries must be finite")
     if vals.size and vals.min() < 0.0:
         raise ValueError("data entries must be nonnegative")
-    pair = _resolve_init(init, F, N, config.rank, config.seed)
+    if sharded:
+        # `data` is this rank's row block: W rows are local,
+        # H is replicated; the init is global (or this rank's W rows)
+        from . import parallel
+        if parallel.dist_info() is None:
+            raise ValueError("sharded=True needs an initialised torch.distributed group")
+        f0, f_global = parallel.column_offsets(F)   # offsets of a 1-D partition
+        counts = parallel.allgather_int(N)
+        if len(set(counts)) != 1:
+            raise ValueError("every rank's row block must have the global column count")
+        K = config.rank
+        if init is None:
+            full = init_factors(f_global, N, K, config.seed)
+            w0, h0 = full.w, full.h
+        else:
+            w0, h0 = (init.w, init.h) if isinstance(init, FactorPair) else init
+        w0 = np.asarray(w0, dtype=np.float64)
+        h0 = np.asarray(h0, dtype=np.float64)
+        if w0.shape == (f_global, K):
+            w0 = w0[f0:f0 + F]
+        if w0.shape != (F, K) or h0.shape != (K, N):
+            raise ValueError(f"init shapes {w0.shape}, {h0.shape} do not match the global "
+                             f"{(f_global, N)} or local {(F, N)} data at rank {K}")
+        w_init, h_init = w0, h0
+    else:
+        pair = _resolve_init(init, F, N, config.rank, config.seed)
+        w_init, h_init = pair.w, pair.h
     ctx = get_context(device, "fp32-sparse")
     with ctx.lock:
+        if sharded:
+            _attach_comm(ctx, f_global)
         ctx.set_csr(*arrays, (F, N))
-        ctx.set_factors(pair.w, pair.h)
+        ctx.set_factors(w_init, h_init)
         params = make_params(config, 0.0, kkt=False, schedule="reference")
         done, converged = ctx.run(params, config.max_outer_iters)
         obj, sec, kk = ctx.trace(done)

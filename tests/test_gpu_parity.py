@@ -169,3 +169,36 @@ def test_sparse_matches_oracle_restatement_and_is_deterministic():
                                    init=(w0, h0))
     got = np.array([t.objective for t in r1.trace])
     assert max_rel(got, obj) <= 1e-4
+
+
+def test_sparse_sharded_entry_with_one_rank_matches_unsharded():
+    """The row-sharded sparse entry (sharded=True: global init sliced by row
+    offsets, NCCL communicator attached) on a 1-rank process group gives the
+    single-GPU result bitwise; the N > 1 decomposition is covered on CPU by
+    tests/test_parallel_gloo.py."""
+    import os
+    import socket
+
+    import scipy.sparse as sp
+    import torch.distributed as dist
+    from paper_2106_15214_b200 import synthetic
+    indptr, idx, vals, shape = synthetic.config5(F=3000, N=500, density=0.02, seed=21)
+    csr = sp.csr_matrix((vals, idx, indptr), shape=shape)
+    w0, h0 = synthetic.uniform_init(shape[0], shape[1], 32, seed=132)
+    cfg = bn.SolverConfig(beta=1.0, rank=32, algorithm="jmm", kappa=0.0, tol=1e-300,
+                          max_outer_iters=12)
+    ref = bn.fit(csr, cfg, init=(w0, h0), dtype="fp32")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        got = bn.fit(csr, cfg, init=(w0, h0), dtype="fp32", sharded=True)
+    finally:
+        dist.destroy_process_group()
+    assert [t.objective for t in got.trace] == [t.objective for t in ref.trace]
+    assert np.array_equal(got.factors.w, ref.factors.w)
+    assert np.array_equal(got.factors.h, ref.factors.h)

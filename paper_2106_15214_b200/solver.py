@@ -396,7 +396,7 @@ def csr_with_csc_view(data):
     indices, perm[j] = CSR position of CSC entry j) -- the deterministic
     column-sum layout of the sparse path."""
     import scipy.sparse as sp
-    m = sp.csr_matrix(data, dtype=np.float32)
+    m = sp.csr_matrix(data, dtype=np.float32, copy=True)
     m.sum_duplicates()
     m.sort_indices()
     F, N = m.shape
@@ -426,12 +426,13 @@ def _run_sparse(data, config, counter, algorithm, *, dtype="fp32", init=None, de
     if (config.sub_iters != 1 or (config.sub_iters_w or 1) != 1
             or (config.sub_iters_h or 1) != 1):
         raise ValueError("the sparse path implements one sub-iteration")
-    arrays, (F, N) = csr_with_csc_view(data)
-    vals = arrays[2]
-    if not np.isfinite(vals).all():
+    import scipy.sparse as sp
+    m = sp.csr_matrix(data, dtype=np.float32)
+    if not np.isfinite(m.data).all():
         raise ValueError("data entries must be finite")
-    if vals.size and vals.min() < 0.0:
+    if m.data.size and m.data.min() < 0.0:
         raise ValueError("data entries must be nonnegative")
+    arrays, (F, N) = csr_with_csc_view(m)
     if sharded:
         # `data` is this rank's row block: W rows are local,
         # H is replicated; the init is global (or this rank's W rows)

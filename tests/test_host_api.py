@@ -65,3 +65,19 @@ def test_scalar_divergence_examples():
     assert bn.beta_divergence(3.0, 1.0, 2.0) == 2.0
     with pytest.raises(bn.DivergenceDomainError):
         bn.beta_divergence(0.0, 1.0, 0.0)
+
+
+def test_sparse_layout_does_not_mutate_the_callers_matrix():
+    """csr_with_csc_view sorts indices on a copy (the reference never mutates
+    its inputs)."""
+    import scipy.sparse as sp
+    from paper_2106_15214_b200.solver import csr_with_csc_view
+    indptr = np.array([0, 3, 5])
+    idx = np.array([2, 0, 1, 1, 0], dtype=np.int32)
+    data = np.array([1., 2., 3., 4., 5.], dtype=np.float32)
+    m = sp.csr_matrix((data, idx, indptr), shape=(2, 3))
+    before = (m.indices.copy(), m.data.copy())
+    (ip, ix, v, cp, ri, pm), shape = csr_with_csc_view(m)
+    assert np.array_equal(m.indices, before[0]) and np.array_equal(m.data, before[1])
+    assert shape == (2, 3) and list(ix) == [0, 1, 2, 0, 1] and list(v) == [2, 3, 1, 5, 4]
+    assert list(cp) == [0, 2, 4, 5] and list(v[pm]) == [2, 5, 3, 4, 1]

@@ -139,6 +139,25 @@ __device__ __forceinline__ void dacc(float x, float y, float zd, float beta, flo
   }
 }
 
+// Z for 8 elements; beta = 1.5 forms two lanes per instruction (FMUL2)
+template <int FBC>
+__device__ __forceinline__ void zpair8(const float* x, const float* y, float beta, float* zn,
+                                       float* zd) {
+#ifndef BNMF_NO_F2
+  if (FBC == FBC_15) {
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      const uint64_t r = f2pack(rsqrt_fast(y[i]), rsqrt_fast(y[i + 1]));
+      f2unpack(f2mul(f2pack(x[i], x[i + 1]), r), zn[i], zn[i + 1]);
+      f2unpack(f2mul(f2pack(y[i], y[i + 1]), r), zd[i], zd[i + 1]);
+    }
+    return;
+  }
+#endif
+#pragma unroll
+  for (int i = 0; i < 8; ++i) zpair<FBC>(x[i], y[i], beta, zn[i], zd[i]);
+}
+
 // Z of one k-step (this thread's 8 columns) as TMEM A operands:
 // [Zn hi | Zn lo | Zd hi | Zd lo], 8 columns each, one 32-column store
 __device__ __forceinline__ void store_z(uint32_t taddr, const float* zn, const float* zd) {
@@ -152,11 +171,21 @@ __device__ __forceinline__ void store_z(uint32_t taddr, const float* zn, const f
 #endif
   float z[32];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < 8; i += 2) {
     z[i] = tf32_trunc(zn[i]);
-    z[8 + i] = zn[i] - z[i];
+    z[i + 1] = tf32_trunc(zn[i + 1]);
     z[16 + i] = tf32_trunc(zd[i]);
+    z[17 + i] = tf32_trunc(zd[i + 1]);
+#ifdef BNMF_NO_F2
+    z[8 + i] = zn[i] - z[i];
+    z[9 + i] = zn[i + 1] - z[i + 1];
     z[24 + i] = zd[i] - z[16 + i];
+    z[25 + i] = zd[i + 1] - z[17 + i];
+#else
+    // the lo parts two at a time (FADD2)
+    f2unpack(f2sub(f2pack(zn[i], zn[i + 1]), f2pack(z[i], z[i + 1])), z[8 + i], z[9 + i]);
+    f2unpack(f2sub(f2pack(zd[i], zd[i + 1]), f2pack(z[16 + i], z[17 + i])), z[24 + i], z[25 + i]);
+#endif
   }
   tmem_st32(taddr, z);
 }
@@ -249,7 +278,18 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
 #define BNMF_PROF_T0(v) const long long v = clock64()
 #define BNMF_PROF_ADD(i, v) if (rec) atomicAdd(&pcs[pbase + (i)], (unsigned long long)(clock64() - (v)))
 #else
+#if defined(BNMF_SPIN_ALL)
+  auto pwait = [&](uint64_t* bar, uint32_t parity, int) { mbar_wait_spin(bar, parity); };
+#elif defined(BNMF_SPIN_MMA)
+  auto pwait = [&](uint64_t* bar, uint32_t parity, int) {
+    if ((threadIdx.x >> 5) == 1) mbar_wait_spin(bar, parity);
+    else mbar_wait(bar, parity);
+  };
+#elif defined(BNMF_NOHINT)
+  auto pwait = [&](uint64_t* bar, uint32_t parity, int) { mbar_wait_nohint(bar, parity); };
+#else
   auto pwait = [&](uint64_t* bar, uint32_t parity, int) { mbar_wait(bar, parity); };
+#endif
   auto pwait_cl = [&](uint64_t* bar, uint32_t parity, int) { mbar_wait(bar, parity); };
 #define BNMF_PROF_T0(v)
 #define BNMF_PROF_ADD(i, v)
@@ -416,13 +456,13 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
     };
     auto s_w = [&](int blk, int u) {
       BNMF_TRACE(3, ns);
-      pwait(&bar_zfull[ns & 1], (ns >> 1) & 1, 3);
-      BNMF_TRACE(4, ns);
       const bool fresh = (blk % FOLD) == 0 && u == 0;
-      if (fresh && blk > 0) pwait(bar_accwfree, ((blk / FOLD) - 1) & 1, 5);
-      tc_fence_after();
       const bool fold_end = (blk % FOLD) == FOLD - 1 || blk == nb - 1;
       const uint32_t zb = tmem + TM_Z + 128 * (ns & 1);
+      pwait(&bar_zfull[ns & 1], (ns >> 1) & 1, 3);
+      BNMF_TRACE(4, ns);
+      if (fresh && blk > 0) pwait(bar_accwfree, ((blk / FOLD) - 1) & 1, 5);
+      tc_fence_after();
       if (elect_one()) {
         const uint64_t bh = dplus(d_hnt, u * 8 * HNT_LBO);
         issue_side<2 * HNT_LBO>(tmem + TM_ACCW, zb, bh, id32, id16, fresh);
@@ -600,18 +640,17 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
           if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(bar_xempty), peer));
           BNMF_TRACE(50, blk);
         }
+        // ratio num / max(den, floor), ^gamma; k >= K has h0 = nrm = 0
+        float r[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int k = 4 * g + i;
-          float v = 0.f;
-          if (k < K) {
-            const float dn = den_ones ? cs2[i] : uden[i];
-            const float r = __fdividef(unum[i], fmaxf(dn, floor_f));
-            const float rg = gam == 1.f ? r : (gam == 0.5f ? sqrtf(r) : powf(r, gam));
-            v = h0[i] * rg * nrm[i];
-          }
-          hv[i] = v;
+        for (int i = 0; i < 4; ++i)
+          r[i] = unum[i] * rcp_fast(fmaxf(den_ones ? cs2[i] : uden[i], floor_f));
+        if (gam != 1.f) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) r[i] = gam == 0.5f ? sqrtf(r[i]) : powf(r[i], gam);
         }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) hv[i] = h0[i] * r[i] * nrm[i];
       } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) hv[i] = n < N ? h0[i] : 0.f;
@@ -683,7 +722,9 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
     int c = 0;   // item counter (Vt / Z buffer c & 1)
     float objb = 0.f;   // objective of the current block (fp32, 32 terms per thread)
     // Vt tile of item c -> registers; the buffer is handed back right away
-    auto load_d = [&](int buf, float* y) { tmem_ld8(lane_base + TM_D + 32 * buf + 8 * g, y); };
+    auto load_d = [&](int buf, float* y) {
+      tmem_ld8(lane_base + TM_D + 32 * buf + 8 * g, y);
+    };
     // Z of item c -> TMEM (buffer free: dfull(c) retired the side products of c - 2)
     auto put_z = [&](int buf, const float* zn, const float* zd) {
       store_z(lane_base + TM_Z + 128 * buf + 32 * g, zn, zd);
@@ -718,8 +759,11 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
       float x[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) x[i] = lds_f32(xa + i * VROWB);
+      if (KAPPA) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) zpair<FBC>(x[i], KAPPA ? y[i] + kappa : y[i], beta, zn[i], zd[i]);
+        for (int i = 0; i < 8; ++i) y[i] += kappa;
+      }
+      zpair8<FBC>(x, y, beta, zn, zd);
       if (!(n0 + BN <= N && (rows_full || 32 * idx + 32 <= FTr))) {
         const bool nok = n0 + row < N;
 #pragma unroll
@@ -750,6 +794,28 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
 #pragma unroll
         for (int i = 0; i < 8; ++i) x[i] = 0.f;
       }
+#ifndef BNMF_NO_F2
+      if (FBC == FBC_15 && n0 + BN <= N && row < FTr) {
+        // beta = 1.5, full tile: Z and the objective two lanes per instruction
+        if (KAPPA) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) y[i] += kappa;
+        }
+        zpair8<FBC>(x, y, beta, zn, zd);
+        const uint64_t two = f2pack(2.f, 2.f);
+        uint64_t acc = 0ull;
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+          const uint64_t sx = f2pack(sqrt_fast(x[i]), sqrt_fast(x[i + 1]));
+          const uint64_t zdp = f2pack(zd[i], zd[i + 1]);
+          const uint64_t dq = f2sub(sx, zdp);
+          acc = f2fma(f2mul(dq, dq), f2fma(two, sx, zdp), acc);
+        }
+        float o0, o1;
+        f2unpack(acc, o0, o1);
+        objb += o0 + o1;
+      } else
+#endif
       if (n0 + BN <= N && row < FTr) {
         float o0 = 0.f, o1 = 0.f;
 #pragma unroll

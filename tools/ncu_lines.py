@@ -6,6 +6,7 @@ import csv, io, subprocess, sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+byinst = len(sys.argv) > 3 and sys.argv[3] == "inst"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
@@ -33,6 +34,6 @@ for r in rows:
 tot = sum(a[0] for a in agg) or 1
 toti = sum(a[1] for a in agg) or 1
 print(f"total samples {tot}, warp-instructions {toti}")
-for s, i, loc, src, st in sorted(agg, reverse=True)[:top]:
+for s, i, loc, src, st in sorted(agg, reverse=True, key=(lambda a: a[1]) if byinst else None)[:top]:
     top3 = ", ".join(f"{k} {v}" for k, v in sorted(st.items(), key=lambda x: -x[1])[:3])
     print(f"{100*s/tot:5.1f}% inst {100*i/toti:5.1f}%  {loc:28s} {src:70s} [{top3}]")

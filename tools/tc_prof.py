@@ -21,7 +21,7 @@ buf = (ctypes.c_longlong * (148 * 48))()
 n = lib.bnmf_tc_prof_read(buf, 148 * 48)
 a = np.array(buf[:n], dtype=np.int64).reshape(-1, 48)
 names = {0: "prod: empty", 11: "prod: total", 12: "mma: dempty",
-         13: "mma: hn", 14: "mma: hp", 15: "mma: zfull", 16: "mma: accfree", 17: "mma: accwfree", 18: "mma: D issue", 19: "mma: side issue", 23: "mma: total",
+         13: "mma: hn", 14: "mma: hp", 15: "mma: zfull", 16: "mma: accfree", 17: "mma: accwfree", 18: "mma: dempty(DL)", 19: "mma: side issue", 23: "mma: total",
          24: "epi: dfull(H)", 25: "epi: full(H)", 26: "epi: dfull(W)", 27: "epi: acch", 28: "epi: xempty",
          29: "epi: xfull", 30: "epi: zempty+wdone", 31: "epi: accw", 32: "epi: U1", 33: "epi: U2", 34: "epi: fold total",
          35: "epi: total"}

@@ -278,7 +278,15 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
 #define BNMF_PROF_T0(v) const long long v = clock64()
 #define BNMF_PROF_ADD(i, v) if (rec) atomicAdd(&pcs[pbase + (i)], (unsigned long long)(clock64() - (v)))
 #else
-#if defined(BNMF_SPIN_ALL)
+#if defined(BNMF_SLEEPW)
+  // back-off per role: producer BNMF_SLEEP_P ns, MMA BNMF_SLEEP_M, epilogue BNMF_SLEEP_E (0 = none)
+  auto pwait = [&](uint64_t* bar, uint32_t parity, int) {
+    const int w = threadIdx.x >> 5;
+    const uint32_t ns = w == 0 ? BNMF_SLEEP_P : (w == 1 ? BNMF_SLEEP_M : BNMF_SLEEP_E);
+    if (ns) mbar_wait_sleep(bar, parity, ns);
+    else mbar_wait(bar, parity);
+  };
+#elif defined(BNMF_SPIN_ALL)
   auto pwait = [&](uint64_t* bar, uint32_t parity, int) { mbar_wait_spin(bar, parity); };
 #elif defined(BNMF_SPIN_MMA)
   auto pwait = [&](uint64_t* bar, uint32_t parity, int) {
@@ -379,11 +387,22 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
   if (warp == 0) {
     // ======================= TMA producer ===================================
     if (lane == 0) {
+#ifndef BNMF_L2PF
+#define BNMF_L2PF 1
+#endif
+      // V rows of block bi + BNMF_L2PF are prefetched into L2 when the stage
+      // loads of block bi are issued: a stage refill (issued when the W items
+      // of the block two back release their slots) then hits L2 instead of
+      // waiting a full DRAM latency
+      for (int bi = 0; bi < BNMF_L2PF && bi < nb; ++bi)
+        for (int j = 0; j < SH; ++j) tma_prefetch_l2_2d(&mapV, col0(bi), row0 + 32 * j);
       for (int bi = 0; bi < nb; ++bi) {
         const int n0 = col0(bi);
         for (int j = 0; j < SH; ++j) {
           uint32_t ph;
           const int s = stage_of(bi, j, ph);
+          if (BNMF_L2PF > 0 && bi + BNMF_L2PF < nb)
+            tma_prefetch_l2_2d(&mapV, col0(bi + BNMF_L2PF), row0 + 32 * j);
           pwait(&bar_empty[s], ph ^ 1, 0);
           mbar_expect_tx(&bar_full[s], STAGE_BYTES);
           tma_load_2d(smem + OFF_STAGE + s * STAGE_BYTES, &mapV, &bar_full[s], n0, row0 + 32 * j);

@@ -79,6 +79,13 @@ __device__ __forceinline__ void mbar_wait_nohint(uint64_t* bar, uint32_t parity)
   while (!mbar_try_nohint(a, parity)) {
   }
 }
+// wait with a nanosleep back-off between probes: for waiters that are not
+// latency critical, so that polling does not take issue slots from the warps
+// doing the work on the same SM sub-partition
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  const uint32_t a = smem_u32(bar);
+  while (!mbar_try(a, parity)) __nanosleep(ns);
+}
 // Wait for the phase with the given parity.  BNMF_WATCHDOG (debug builds)
 // turns a lost arrival into a trap instead of a hang.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {

@@ -278,26 +278,7 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
 #define BNMF_PROF_T0(v) const long long v = clock64()
 #define BNMF_PROF_ADD(i, v) if (rec) atomicAdd(&pcs[pbase + (i)], (unsigned long long)(clock64() - (v)))
 #else
-#if defined(BNMF_SLEEPW)
-  // back-off per role: producer BNMF_SLEEP_P ns, MMA BNMF_SLEEP_M, epilogue BNMF_SLEEP_E (0 = none)
-  auto pwait = [&](uint64_t* bar, uint32_t parity, int) {
-    const int w = threadIdx.x >> 5;
-    const uint32_t ns = w == 0 ? BNMF_SLEEP_P : (w == 1 ? BNMF_SLEEP_M : BNMF_SLEEP_E);
-    if (ns) mbar_wait_sleep(bar, parity, ns);
-    else mbar_wait(bar, parity);
-  };
-#elif defined(BNMF_SPIN_ALL)
-  auto pwait = [&](uint64_t* bar, uint32_t parity, int) { mbar_wait_spin(bar, parity); };
-#elif defined(BNMF_SPIN_MMA)
-  auto pwait = [&](uint64_t* bar, uint32_t parity, int) {
-    if ((threadIdx.x >> 5) == 1) mbar_wait_spin(bar, parity);
-    else mbar_wait(bar, parity);
-  };
-#elif defined(BNMF_NOHINT)
-  auto pwait = [&](uint64_t* bar, uint32_t parity, int) { mbar_wait_nohint(bar, parity); };
-#else
   auto pwait = [&](uint64_t* bar, uint32_t parity, int) { mbar_wait(bar, parity); };
-#endif
   auto pwait_cl = [&](uint64_t* bar, uint32_t parity, int) { mbar_wait(bar, parity); };
 #define BNMF_PROF_T0(v)
 #define BNMF_PROF_ADD(i, v)

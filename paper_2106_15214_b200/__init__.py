@@ -34,6 +34,7 @@ from .solver import (
 )
 from .updates import Algorithm, OpCounter, UpdateKind
 from . import parallel  # noqa: F401  (N-column sharding helpers)
+from . import harness, matrixio  # noqa: F401  (multi-seed harness, matrix IO; cli.py uses both)
 
 __version__ = "0.1.0"
 

@@ -53,7 +53,10 @@ constexpr int SP_SEG = 2048;   // nonzeros per column segment (pass B1)
 constexpr int SP_HEAVY = 2048;
 constexpr int SP_TILE = 131072;
 constexpr int SP_SEG_H = 512;  // heavy-column segments (more warps per tile)
-constexpr int SP_U = 4;        // nonzeros per 8-lane group in flight
+#ifndef BNMF_SP_U
+#define BNMF_SP_U 4
+#endif
+constexpr int SP_U = BNMF_SP_U;   // nonzeros per 8-lane group in flight
 
 struct SpArgs {
   int F, N, K, KL;
@@ -254,8 +257,23 @@ __global__ void sp_pass_b2(SpArgs a, const RunState* st, int slot) {
     const int s0 = a.colseg[n], s1 = a.colseg[n + 1];
     float v = a.part[size_t(a.seglist[s0]) * a.KL + k];
     if (s1 - s0 > 1) {
+      // same left-to-right order as a plain loop (bitwise identical), but the
+      // segment ids and partials of 8 segments are loaded before any is added:
+      // a Zipf-heavy column has thousands of segments, and a dependent
+      // id -> partial -> add chain per segment made this pass latency bound
       double acc = double(v);
-      for (int s = s0 + 1; s < s1; ++s) acc += double(a.part[size_t(a.seglist[s]) * a.KL + k]);
+      int s = s0 + 1;
+      for (; s + 8 <= s1; s += 8) {
+        int id[8];
+        float pv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) id[i] = a.seglist[s + i];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pv[i] = a.part[size_t(id[i]) * a.KL + k];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc += double(pv[i]);
+      }
+      for (; s < s1; ++s) acc += double(a.part[size_t(a.seglist[s]) * a.KL + k]);
       v = float(acc);
     }
     a.num[t] = v;

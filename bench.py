@@ -257,6 +257,7 @@ def main():
     with clocks:
         ms = ctx.step_timed(args.steps)
     pass_ms, pass_samples = ctx.pass_time()
+    ctx.set_profiling(False)   # the e2e leg below runs without per-pass events
     done, _ = ctx.sync()
     obj, _, _ = ctx.trace(done)
     launches = ctx.launches_per_iter()
@@ -279,22 +280,27 @@ def main():
                                 kappa=kappa, max_outer_iters=max(1, args.warmup))
         bn.fit(vp, cfg_w, init=(w0, h0), dtype=c["dtype"], kkt=False, schedule=args.schedule,
                sharded=world > 1)
-        if world > 1:
-            torch.distributed.barrier()
-        t0 = time.perf_counter()
-        res = bn.fit(vp, cfg_e, init=(w0, h0), dtype=c["dtype"], kkt=False,
-                     schedule=args.schedule, sharded=world > 1)
-        _ = res.trace[-1].objective
-        te = time.perf_counter() - t0
-        te = float(parallel.allreduce_scalars([te], "max")[0]) if world > 1 else te
+        # median of three timed calls: the host side (fresh fp64 result arrays, pageable
+        # copies of the init and factors) varies by +-30 % from call to call
+        tes = []
+        for _rep in range(3):
+            if world > 1:
+                torch.distributed.barrier()
+            t0 = time.perf_counter()
+            res = bn.fit(vp, cfg_e, init=(w0, h0), dtype=c["dtype"], kkt=False,
+                         schedule=args.schedule, sharded=world > 1)
+            _ = res.trace[-1].objective
+            te = time.perf_counter() - t0
+            tes.append(float(parallel.allreduce_scalars([te], "max")[0]) if world > 1 else te)
+        te = statistics.median(tes)
         h2d = v.nbytes + w0.nbytes + h0.nbytes
         d2h = res.factors.w.nbytes + res.factors.h.nbytes + 24 * args.steps
         e2e = {"value": args.steps / te, "unit": "iterations/s",
                "h2d_bytes_per_step": int(h2d * world / args.steps),
                "d2h_bytes_per_step": int(d2h * world / args.steps),
-               "note": "one fit() call on pinned host V after one untimed warm-up call: "
-                       f"upload, host-side domain checks, {args.steps} iterations, download of "
-                       "W, H and trace"}
+               "note": "median of 3 fit() calls on pinned host V after one untimed warm-up "
+                       f"call; each: upload, host-side domain checks, {args.steps} iterations, "
+                       "download of W, H and trace", "calls_s": [round(t, 4) for t in tes]}
 
     if rank != 0:
         return

@@ -111,21 +111,18 @@ __device__ __forceinline__ float group_sum(float v) {
 
 // ---- pass A: rows --------------------------------------------------------
 template <int KPL>
-__global__ void __launch_bounds__(SP_THREADS) sp_pass_a(SpArgs a, const RunState* st, int slot) {
+__global__ void __launch_bounds__(SP_THREADS, 3) sp_pass_a(SpArgs a, const RunState* st, int slot) {
   if (!iter_active(st, slot)) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane >> 3, sl = lane & 7, k0 = sl * KPL;
   const int KL = a.KL;
-  double cs[KPL], sq[KPL];
-#pragma unroll
-  for (int i = 0; i < KPL; ++i) { cs[i] = 0.0; sq[i] = 0.0; }
-  __shared__ double red[SP_WARPS][2 * SP_KMAX];
-  double rinv[KPL];
-#pragma unroll
-  for (int i = 0; i < KPL; ++i) {
-    const int k = k0 + i;
-    rinv[i] = k < a.K ? 1.0 / fmax(a.denw[k], a.sc.floor) : 0.0;
-  }
+  // 1 / max(rowsum H~, floor) per k in shared memory (not 8 fp64 registers per
+  // thread: pass A is latency bound on the H~ gathers, and registers set how
+  // many rows are in flight); the W_p column statistics are a separate pass
+  __shared__ double s_rinv[SP_KMAX];
+  for (int k = threadIdx.x; k < KL; k += blockDim.x)
+    s_rinv[k] = k < a.K ? 1.0 / fmax(a.denw[k], a.sc.floor) : 0.0;
+  __syncthreads();
   for (int f = blockIdx.x * SP_WARPS + warp; f < a.F; f += gridDim.x * SP_WARPS) {
     float w[KPL], num[KPL];
     ld_row<KPL>(a.Wt + size_t(f) * KL + k0, w);
@@ -170,27 +167,41 @@ __global__ void __launch_bounds__(SP_THREADS) sp_pass_a(SpArgs a, const RunState
         const int k = k0 + i;
         wn[i] = 0.f;
         if (k < a.K) {
-          const double r = double(num[i]) * rinv[i];
+          const double r = double(num[i]) * s_rinv[k];
           wn[i] = float(double(w[i]) * apply_exponent<double>(r, a.sc.gamma));
-          cs[i] += double(wn[i]);
-          sq[i] += double(wn[i]) * double(wn[i]);
         }
       }
       st_row<KPL>(a.Wp + size_t(f) * KL + k0, wn);
     }
   }
-  if (grp == 0)
-#pragma unroll
-    for (int i = 0; i < KPL; ++i) {
-      red[warp][k0 + i] = cs[i];
-      red[warp][SP_KMAX + k0 + i] = sq[i];
+}
+
+// W_p column statistics: per-block fp64 partials of colsum and sum of squares
+// over a fixed row assignment (block b: rows b*RP + r, stepping gridDim*RP),
+// reduced in a fixed order -> deterministic
+__global__ void __launch_bounds__(SP_THREADS) sp_colstats(SpArgs a, const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  const int KL = a.KL, RP = SP_THREADS / KL;
+  const int k = threadIdx.x % KL, r = threadIdx.x / KL;
+  double cs = 0.0, sq = 0.0;
+  if (k < a.K && r < RP)
+    for (int f = blockIdx.x * RP + r; f < a.F; f += gridDim.x * RP) {
+      const double w = double(a.Wp[size_t(f) * KL + k]);
+      cs += w;
+      sq += w * w;
     }
+  __shared__ double red[2][SP_THREADS];
+  red[0][threadIdx.x] = cs;
+  red[1][threadIdx.x] = sq;
   __syncthreads();
-  for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
+  if (threadIdx.x < a.K) {
     double s0 = 0.0, s1 = 0.0;
-    for (int w = 0; w < SP_WARPS; ++w) { s0 += red[w][k]; s1 += red[w][SP_KMAX + k]; }
-    a.pa[size_t(blockIdx.x) * 2 * a.K + k] = s0;
-    a.pa[size_t(blockIdx.x) * 2 * a.K + a.K + k] = s1;
+    for (int rr = 0; rr < RP; ++rr) {
+      s0 += red[0][rr * KL + threadIdx.x];
+      s1 += red[1][rr * KL + threadIdx.x];
+    }
+    a.pa[size_t(blockIdx.x) * 2 * a.K + threadIdx.x] = s0;
+    a.pa[size_t(blockIdx.x) * 2 * a.K + a.K + threadIdx.x] = s1;
   }
 }
 
@@ -363,11 +374,19 @@ __global__ void __launch_bounds__(SP_THREADS) sp_pass_c(SpArgs a, const RunState
 __global__ void sp_reduce_a(const double* pa, int G, int K, double* comm, const RunState* st,
                             int slot) {
   if (!iter_active(st, slot)) return;
-  for (int i = threadIdx.x; i < 2 * K; i += blockDim.x) {
-    double s = 0.0;
-    for (int g = 0; g < G; ++g) s += pa[size_t(g) * 2 * K + i];
-    comm[i] = s;
+  // block i sums output i: thread t takes partials t, t + 256, ... in order,
+  // then a fixed shared-memory tree (deterministic)
+  __shared__ double red[256];
+  const int i = blockIdx.x;
+  double s = 0.0;
+  for (int g = threadIdx.x; g < G; g += blockDim.x) s += pa[size_t(g) * 2 * K + i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) comm[i] = red[0];
 }
 // DenH = colsum(W_p), norms = sqrt(sum_f W_p^2)  (after the allreduce)
 __global__ void sp_post_a(const double* comm, int K, double* denh, double* norms,
@@ -496,7 +515,7 @@ struct SparseEngine : EngineBase {
   int64_t tr_cap = 0;
   RunState* st = nullptr;
   RunState* st_host = nullptr;
-  int GA = 1, GB1 = 1, GB3 = 1, nsm = 148;
+  int GA = 1, GB1 = 1, GB3 = 1, GS = 1, nsm = 148;
   bnmf_params p{};
   Scalars sc{};
   bool begun = false;
@@ -655,7 +674,8 @@ struct SparseEngine : EngineBase {
       SCK(cudaMalloc(&denw, K * sizeof(double)));
       SCK(cudaMalloc(&denh, K * sizeof(double)));
       SCK(cudaMalloc(&norms, K * sizeof(double)));
-      SCK(cudaMalloc(&pa, size_t(GA) * 2 * K * sizeof(double)));
+      GS = std::max(1, std::min((F + SP_THREADS / KL - 1) / (SP_THREADS / KL), nsm * 4));
+      SCK(cudaMalloc(&pa, size_t(GS) * 2 * K * sizeof(double)));
       SCK(cudaMalloc(&pb, size_t(GB3) * K * sizeof(double)));
       SCK(cudaMalloc(&pc, size_t(GA) * sizeof(double)));
       SCK(cudaMalloc(&comm, (2 * K + 8) * sizeof(double)));
@@ -775,9 +795,10 @@ struct SparseEngine : EngineBase {
     SpArgs a = args();
     begin_iter<<<1, 1, 0, stream>>>(st, slot);
     dispatch(0, a, slot);
-    sp_reduce_a<<<1, 256, 0, stream>>>(pa, GA, K, comm, st, slot);
+    sp_colstats<<<GS, SP_THREADS, 0, stream>>>(a, st, slot);
+    sp_reduce_a<<<2 * K, 256, 0, stream>>>(pa, GS, K, comm, st, slot);
     SCK(cudaGetLastError());
-    launches += 3;
+    launches += 4;
     if (int rc = allreduce(comm, 2 * size_t(K), ncclDouble)) return rc;
     sp_post_a<<<1, 128, 0, stream>>>(comm, K, denh, norms, st, slot);
     dispatch(1, a, slot);

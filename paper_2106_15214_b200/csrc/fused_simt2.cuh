@@ -1,0 +1,356 @@
+// Register-tiled SIMT form of the fused pass (fp32, any F, K <= 64), used for
+// the shapes outside the tcgen05 kernel's limits (configs 2 and 3: F > 256,
+// K > 16).  Same contract as fused_pass_tc / fused_common.cuh, split in two
+// kernels so that each keeps its accumulators in registers:
+//
+//   fs2::hpass  one CTA per 32-column block, all F rows in 64-row chunks:
+//               Vt_{p-1} = Wa H~_{p-1} + kappa, Z by the beta rule, and the
+//               H-side sums chi1^T Zn / chi2^T Zd -> H_p, H~_p = H_p norms_p
+//               (updates.py:223-235 / 173-181, solver.py:167-171);
+//   fs2::wpass  grid (64-row chunk, column segment): Vt_p = W~_p H~_p + kappa,
+//               the objective of iterate p (solver.py:304-309) and the W-side
+//               sums Zn H~_p^T, Zd H~_p^T of iteration p+1 (updates.py:203-220),
+//               held in fp64 registers over the whole segment and written
+//               once to the segment's slab part[seg][2][F][K].
+//
+// V is read twice per iteration; at configs 2 and 3 it is L2-resident
+// (34 / 67 MB < 126 MB), so the second read is served by L2.  Every thread
+// owns a 4-row x 2-column tile of Vt (columns tn and tn+16, so the 16-byte
+// loads of the H rows are bank-conflict free with a row stride = 4 mod 8).
+// Per chunk/step the sums are fp32 and are folded into fp64 registers; all
+// orders are fixed, so results are bitwise reproducible.
+#pragma once
+
+#include "fused_common.cuh"
+#include "simt_kernels.cuh"
+
+namespace bnmf {
+namespace fs2 {
+
+constexpr int THREADS = 256;
+constexpr int TF = 64;        // rows per chunk
+constexpr int NC = 32;        // columns per block / step
+constexpr int TFP = TF + 4;   // row stride of the transposed Z tile
+
+__host__ __device__ inline int kr4(int K) { return (K + 3) & ~3; }
+// row stride of the row-major factor tiles: >= K rounded to 4, = 4 (mod 8)
+__host__ __device__ inline int krs(int K) { int r = kr4(K); return (r & 7) == 4 ? r : r + 4; }
+__host__ __device__ inline int kj_of(int K) { return K <= 32 ? 1 : 2; }
+
+__host__ inline size_t h_smem(int K) {
+  const int rs = krs(K), ks = 32 * kj_of(K);
+  // Hp [NC][rs] (+32 slack), then Ws [TF][rs], C1s/C2s [TF][ks], Zn/Zd [TF][NC],
+  // which the group sums Red [4][2][ks][NC] alias
+  const size_t tiles = size_t(TF) * rs + 2 * size_t(TF) * ks + 2 * size_t(TF) * NC;
+  const size_t red = size_t(8) * ks * NC;
+  return sizeof(float) * (size_t(NC) * rs + 32 + (tiles > red ? tiles : red));
+}
+__host__ inline size_t w_smem(int K) {
+  const int rs = krs(K);
+  // Ws [TF][rs], Hs [NC][rs] (+64 slack), ZnT/ZdT [NC][TFP]
+  return sizeof(float) * (size_t(TF) * rs + size_t(NC) * rs + 64 + 2 * size_t(NC) * TFP);
+}
+
+// y[i][j] = sum_k Ws[r_i][k] * Hs[c_j][k], rows r_i = 4 tf + i, columns
+// c_0 = tn, c_1 = tn + 16; k in ascending order (same order as the SIMT twin)
+__device__ __forceinline__ void vt_tile(const float* Ws, const float* Hs, int rs, int kr, int tf,
+                                        int tn, float (&y)[4][2]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { y[i][0] = 0.f; y[i][1] = 0.f; }
+  const float* h0p = Hs + tn * rs;
+  const float* h1p = Hs + (tn + 16) * rs;
+  const float* wp = Ws + (tf * 4) * rs;
+#pragma unroll 2
+  for (int k = 0; k < kr; k += 4) {
+    const float4 h0 = *reinterpret_cast<const float4*>(h0p + k);
+    const float4 h1 = *reinterpret_cast<const float4*>(h1p + k);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 w = *reinterpret_cast<const float4*>(wp + i * rs + k);
+      y[i][0] = fmaf(w.x, h0.x, y[i][0]); y[i][1] = fmaf(w.x, h1.x, y[i][1]);
+      y[i][0] = fmaf(w.y, h0.y, y[i][0]); y[i][1] = fmaf(w.y, h1.y, y[i][1]);
+      y[i][0] = fmaf(w.z, h0.z, y[i][0]); y[i][1] = fmaf(w.z, h1.z, y[i][1]);
+      y[i][0] = fmaf(w.w, h0.w, y[i][0]); y[i][1] = fmaf(w.w, h1.w, y[i][1]);
+    }
+  }
+}
+
+// rows [0, rows) of a row-major K-wide global block -> smem row stride rs,
+// zero-filled to width `width` and past `valid` rows
+__device__ __forceinline__ void load_tile(float* dst, const float* __restrict__ src, int rows,
+                                          int valid, int K, int rs, int width) {
+  for (int i = threadIdx.x; i < rows * width; i += THREADS) {
+    const int r = i / width, k = i - r * width;
+    dst[r * rs + k] = (r < valid && k < K) ? src[(size_t)r * K + k] : 0.f;
+  }
+}
+
+template <int BC, int KJ>
+__global__ void __launch_bounds__(THREADS)
+hpass(FusedArgs a, const RunState* st, int slot, int p_override) {
+  if (p_override < 0 && !iter_active(st, slot)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int KS = 32 * KJ;
+  constexpr bool DEN = BC != BC_1;   // beta = 1: den = colsum(C2) (updates.py:133-137)
+  const int K = a.K, F = a.F, N = a.N, rs = krs(K), kr = kr4(K);
+  float* Hp = reinterpret_cast<float*>(smem_raw);   // [NC][rs]
+  float* Ws = Hp + NC * rs + 32;                    // [TF][rs]
+  float* C1s = Ws + TF * rs;                        // [TF][KS]
+  float* C2s = C1s + TF * KS;                       // [TF][KS]
+  float* Zn = C2s + TF * KS;                        // [TF][NC]
+  float* Zd = Zn + TF * NC;
+
+  const int par = iter_parity(st, slot, p_override);
+  const float* Hprev = a.Hbuf[par ^ 1];
+  float* Hnew = a.Hout[par];
+  const float* Wa = a.algorithm == 0 ? a.Wt2[par ^ 1] : a.Wn;
+  const float kappa = float(a.sc.kappa), beta = float(a.sc.beta);
+  const int tid = threadIdx.x, tn = tid & 15, tf = tid >> 4;
+  const int n0 = blockIdx.x * NC;
+  const int valid_n = min(NC, N - n0);
+
+  load_tile(Hp, Hprev + (size_t)n0 * K, NC, valid_n, K, rs, kr);
+
+  // per chunk: 4 row groups of 16 rows x (4 k x 4 n tiles); the group sums
+  // meet in Red (aliasing the chunk's tiles) and are folded into fp64 in a
+  // fixed order.  Thread tid owns the (k, n) outputs e = tid + 256 m.
+  constexpr int NOUT = KS * NC / THREADS;
+  float* Red = Ws;                                  // [4][2][KS][NC] after the sums
+  const int fg = tid >> 6, t = tid & 63;
+  const int k4 = (t >> 3) * 4, n4 = (t & 7) * 4;
+  double accn[NOUT], accd[NOUT];
+#pragma unroll
+  for (int m = 0; m < NOUT; ++m) { accn[m] = 0.0; accd[m] = 0.0; }
+
+  for (int f0 = 0; f0 < F; f0 += TF) {
+    const int vf = min(TF, F - f0);
+    __syncthreads();
+    load_tile(Ws, Wa + (size_t)f0 * K, TF, vf, K, rs, kr);
+    load_tile(C1s, a.C1 + (size_t)f0 * K, TF, vf, K, KS, KS);
+    if (DEN) load_tile(C2s, a.C2 + (size_t)f0 * K, TF, vf, K, KS, KS);
+    float x[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int f = tf * 4 + i, n = tn + 16 * j;
+        x[i][j] = (f < vf && n < valid_n) ? a.V[(size_t)(f0 + f) * a.ldv + n0 + n] : 0.f;
+      }
+    __syncthreads();
+    float y[4][2];
+    vt_tile(Ws, Hp, rs, kr, tf, tn, y);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int f = tf * 4 + i, n = tn + 16 * j;
+        float zn = 0.f, zd = 0.f;
+        if (f < vf && n < valid_n) bases32<BC>(x[i][j], y[i][j] + kappa, beta, zn, zd);
+        Zn[f * NC + n] = zn;
+        if (DEN) Zd[f * NC + n] = zd;
+      }
+    __syncthreads();
+    // group sums: S[k][n] = sum_{f in group} C1[f][k] Zn[f][n]  (and C2 / Zd)
+    float sn[KJ][4][4], sd[KJ][4][4];
+#pragma unroll
+    for (int j = 0; j < KJ; ++j)
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) { sn[j][u][v] = 0.f; sd[j][u][v] = 0.f; }
+    const int fe = min(16, vf - fg * 16);
+#pragma unroll 2
+    for (int ff = 0; ff < fe; ++ff) {
+      const int f = fg * 16 + ff;
+      const float4 z4 = *reinterpret_cast<const float4*>(Zn + f * NC + n4);
+      const float z[4] = {z4.x, z4.y, z4.z, z4.w};
+      float d[4] = {0.f, 0.f, 0.f, 0.f};
+      if (DEN) {
+        const float4 d4 = *reinterpret_cast<const float4*>(Zd + f * NC + n4);
+        d[0] = d4.x; d[1] = d4.y; d[2] = d4.z; d[3] = d4.w;
+      }
+#pragma unroll
+      for (int j = 0; j < KJ; ++j) {
+        const float4 c4 = *reinterpret_cast<const float4*>(C1s + f * KS + k4 + 32 * j);
+        const float c[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) sn[j][u][v] = fmaf(c[u], z[v], sn[j][u][v]);
+        if (DEN) {
+          const float4 e4 = *reinterpret_cast<const float4*>(C2s + f * KS + k4 + 32 * j);
+          const float e[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) sd[j][u][v] = fmaf(e[u], d[v], sd[j][u][v]);
+        }
+      }
+    }
+    __syncthreads();   // tiles dead: Red aliases them
+    float* rn = Red + (size_t)fg * 2 * KS * NC;
+    float* rd = rn + KS * NC;
+#pragma unroll
+    for (int j = 0; j < KJ; ++j)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k4 + 32 * j + u;
+        *reinterpret_cast<float4*>(rn + k * NC + n4) =
+            make_float4(sn[j][u][0], sn[j][u][1], sn[j][u][2], sn[j][u][3]);
+        if (DEN)
+          *reinterpret_cast<float4*>(rd + k * NC + n4) =
+              make_float4(sd[j][u][0], sd[j][u][1], sd[j][u][2], sd[j][u][3]);
+      }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < NOUT; ++m) {
+      const int e = tid + THREADS * m;
+      float tn_ = 0.f, td_ = 0.f;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        tn_ += Red[(size_t)g * 2 * KS * NC + e];
+        if (DEN) td_ += Red[(size_t)g * 2 * KS * NC + KS * NC + e];
+      }
+      accn[m] += double(tn_);
+      if (DEN) accd[m] += double(td_);
+    }
+  }
+  // H_p = H~_{p-1} * ratio^gamma ; H~_p = H_p * norms_p
+#pragma unroll
+  for (int m = 0; m < NOUT; ++m) {
+    const int e = tid + THREADS * m, k = e / NC, n = e - k * NC;
+    if (k < K && n < valid_n) {
+      const double den = DEN ? accd[m] : a.csum2[k];
+      const double r = accn[m] / fmax(den, a.sc.floor);
+      const double h = double(Hp[n * rs + k]) * apply_exponent<double>(r, a.sc.gamma);
+      Hnew[(size_t)(n0 + n) * K + k] = float(h * a.norms[k]);
+    }
+  }
+}
+
+template <int BC, int KJ>
+__global__ void __launch_bounds__(THREADS)
+wpass(FusedArgs a, const RunState* st, int slot, int p_override, int seg_cols) {
+  if (p_override < 0 && !iter_active(st, slot)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int K = a.K, F = a.F, N = a.N, rs = krs(K), kr = kr4(K);
+  float* Ws = reinterpret_cast<float*>(smem_raw);   // [TF][rs]
+  float* Hs = Ws + TF * rs;                         // [NC][rs] (+64 slack for the k-pair reads)
+  float* ZnT = Hs + NC * rs + 64;                   // [NC][TFP]
+  float* ZdT = ZnT + NC * TFP;
+  __shared__ double red[THREADS / 32];
+
+  const int par = iter_parity(st, slot, p_override);
+  const float* Wt = a.Wt2[par];                             // W~_p
+  const float* Hc = a.do_h ? a.Hout[par] : a.Hbuf[par];     // H~_p
+  const float kappa = float(a.sc.kappa), beta = float(a.sc.beta);
+  const int tid = threadIdx.x, tn = tid & 15, tf = tid >> 4;
+  const int cf = (tid >> 4) * 4, ck = (tid & 15) * 2;   // W-sum tile: 4 rows x k pair
+  const int f0 = blockIdx.x * TF, vf = min(TF, F - f0);
+  const int nbeg = blockIdx.y * seg_cols, nend = min(N, nbeg + seg_cols);
+
+  load_tile(Ws, Wt + (size_t)f0 * K, TF, vf, K, rs, kr);
+
+  double pn[KJ][4][2], pd[KJ][4][2];
+#pragma unroll
+  for (int j = 0; j < KJ; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { pn[j][i][0] = pn[j][i][1] = 0.0; pd[j][i][0] = pd[j][i][1] = 0.0; }
+  double obj = 0.0;
+
+  for (int n0 = nbeg; n0 < nend; n0 += NC) {
+    const int valid_n = min(NC, nend - n0);
+    __syncthreads();
+    load_tile(Hs, Hc + (size_t)n0 * K, NC, valid_n, K, rs, kr);
+    float x[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int f = tf * 4 + i, n = tn + 16 * j;
+        x[i][j] = (f < vf && n < valid_n) ? a.V[(size_t)(f0 + f) * a.ldv + n0 + n] : 0.f;
+      }
+    __syncthreads();
+    float y[4][2];
+    vt_tile(Ws, Hs, rs, kr, tf, tn, y);
+    float zn[4][2], zd[4][2], ob = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        zn[i][j] = 0.f; zd[i][j] = 0.f;
+        const int f = tf * 4 + i, n = tn + 16 * j;
+        if (f < vf && n < valid_n) {
+          const float yy = y[i][j] + kappa;
+          ob += divergence32<BC>(x[i][j], yy, beta);
+          bases32<BC>(x[i][j], yy, beta, zn[i][j], zd[i][j]);
+        }
+      }
+    obj += double(ob);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int n = tn + 16 * j;
+      *reinterpret_cast<float4*>(ZnT + n * TFP + tf * 4) =
+          make_float4(zn[0][j], zn[1][j], zn[2][j], zn[3][j]);
+      *reinterpret_cast<float4*>(ZdT + n * TFP + tf * 4) =
+          make_float4(zd[0][j], zd[1][j], zd[2][j], zd[3][j]);
+    }
+    __syncthreads();
+    // P[f][k] += sum_n Zn[f][n] H~[n][k]  (and Zd)
+    float sn[KJ][4][2], sd[KJ][4][2];
+#pragma unroll
+    for (int j = 0; j < KJ; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { sn[j][i][0] = sn[j][i][1] = 0.f; sd[j][i][0] = sd[j][i][1] = 0.f; }
+#pragma unroll 4
+    for (int n = 0; n < valid_n; ++n) {
+      const float4 z = *reinterpret_cast<const float4*>(ZnT + n * TFP + cf);
+      const float4 d = *reinterpret_cast<const float4*>(ZdT + n * TFP + cf);
+      const float zz[4] = {z.x, z.y, z.z, z.w}, dd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+      for (int j = 0; j < KJ; ++j) {
+        const float2 h = *reinterpret_cast<const float2*>(Hs + n * rs + ck + 32 * j);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          sn[j][i][0] = fmaf(zz[i], h.x, sn[j][i][0]); sn[j][i][1] = fmaf(zz[i], h.y, sn[j][i][1]);
+          sd[j][i][0] = fmaf(dd[i], h.x, sd[j][i][0]); sd[j][i][1] = fmaf(dd[i], h.y, sd[j][i][1]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < KJ; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          pn[j][i][v] += double(sn[j][i][v]);
+          pd[j][i][v] += double(sd[j][i][v]);
+        }
+  }
+  // this segment's slab: rows [f0, f0+vf) of part[seg][2][F][K]
+  double* slab = a.part + (size_t)blockIdx.y * 2 * F * K;
+#pragma unroll
+  for (int j = 0; j < KJ; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int f = cf + i, k = ck + 32 * j + v;
+        if (f < vf && k < K) {
+          const size_t idx = (size_t)(f0 + f) * K + k;
+          slab[idx] = pn[j][i][v];
+          slab[(size_t)F * K + idx] = pd[j][i][v];
+        }
+      }
+  for (int o = 16; o > 0; o >>= 1) obj += __shfl_down_sync(0xffffffffu, obj, o);
+  if ((tid & 31) == 0) red[tid >> 5] = obj;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < THREADS / 32; ++w) t += red[w];
+    a.opart[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+}  // namespace fs2
+}  // namespace bnmf

@@ -8,7 +8,8 @@
 //   finish_iter       trace row p + stop rule (solver.py:309-319)
 //   fused_update      W_{p+1}, norms, W~_{p+1}, chi maps for pass p+1
 // The pass kernel is the tcgen05 kernel (fused_pass_tc, see fused_tc_kernel.cuh)
-// when its shape limits hold, else the SIMT twin (fused_simt.cuh).
+// when its shape limits hold, else the register-tiled SIMT pair fs2::hpass +
+// fs2::wpass (fused_simt2.cuh).
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -20,6 +21,7 @@
 
 #include "engine.h"
 #include "fused_simt.cuh"
+#include "fused_simt2.cuh"
 #include "fused_tc_kernel.cuh"
 #include "small_kernels.cuh"
 
@@ -36,9 +38,9 @@ struct FusedState {
   double* csum2 = nullptr;
   double* part = nullptr;
   double* opart = nullptr;
-  int G = 0;
   int bc = BC_GEN;
-  size_t smem = 0;
+  // SIMT pair: wpass grid (s2_rc row chunks x s2_S column segments)
+  int s2_rc = 0, s2_S = 0, s2_seg = 0;
   // tensor-core pass
   bool tc = false;
   int tc_grid = 0;
@@ -106,11 +108,6 @@ bool fused_supported(int dtype, int F, int K, int algorithm, int L, int Lw, int 
   return Lw == 1 && Lh == 1;
 }
 
-static size_t simt_smem(int K) {
-  int ks = kstride(K);
-  return size_t(2 * ST_NC * ks + 3 * ST_TF * ks + 2 * ST_TF * (ST_NC + 1)) * sizeof(float);
-}
-
 int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
   FusedState* fs = new FusedState;
   *out = fs;
@@ -125,12 +122,18 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
   FCK(cudaMalloc(&fs->C2, fk * sizeof(float)));
   FCK(cudaMalloc(&fs->norms, io.K * sizeof(double)));
   FCK(cudaMalloc(&fs->csum2, io.K * sizeof(double)));
-  int nblocks = (io.N + ST_NC - 1) / ST_NC;
-  fs->G = std::max(1, std::min(nblocks, 2 * 148));
-  fs->smem = simt_smem(io.K);
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  {
+    // wpass: about two CTAs per SM, column segments in whole 32-column steps
+    const int ncb = (io.N + fs2::NC - 1) / fs2::NC;
+    fs->s2_rc = (io.F + fs2::TF - 1) / fs2::TF;
+    int S = std::max(1, std::min(ncb, (2 * nsm + fs->s2_rc - 1) / fs->s2_rc));
+    const int steps = (ncb + S - 1) / S;
+    fs->s2_seg = steps * fs2::NC;
+    fs->s2_S = (io.N + fs->s2_seg - 1) / fs->s2_seg;
+  }
   const char* force_simt = getenv("BNMF_FUSED_SIMT");
   fs->tc = fused_tc_shape_ok(io.F, io.K) && encode_fn() != nullptr &&
            !(force_simt && force_simt[0] == '1');
@@ -162,7 +165,8 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
     }
     fs->tc_grid = fs->tc_cl * std::max(1, std::min(nb, clusters));
   }
-  int gmax = std::max(fs->G, fs->tc_grid);
+  int gmax = std::max(fs->tc_grid, fs->s2_S);
+  const int gobj = std::max(gmax, fs->s2_S * fs->s2_rc);
   const char* prof_env = getenv("BNMF_TC_PROF");
   if (fs->tc && prof_env && prof_env[0] == '1') {
     const size_t np = size_t(fs->tc_grid) * 48 + 3 * 4096;
@@ -171,7 +175,7 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
     g_last_tc = fs;
   }
   FCK(cudaMalloc(&fs->part, size_t(gmax) * 2 * fk * sizeof(double)));
-  FCK(cudaMalloc(&fs->opart, size_t(gmax) * sizeof(double)));
+  FCK(cudaMalloc(&fs->opart, size_t(gobj) * sizeof(double)));
   if (fs->tc) {
     // V stages: [32 rows x 132 columns] boxes, unswizzled; the 4 extra
     // columns pad the SMEM rows to 528 B (conflict-free in both phases)
@@ -221,13 +225,29 @@ static FusedArgs make_args(FusedState* fs, const FusedIO& io, int do_h) {
   return a;
 }
 
+template <int BC, int KJ>
+static cudaError_t launch_simt2(FusedState* fs, const FusedArgs& a, const FusedIO& io, int slot,
+                                int p_override) {
+  if (a.do_h) {
+    auto hk = fs2::hpass<BC, KJ>;
+    const int hs = int(fs2::h_smem(io.K));
+    cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, hs);
+    hk<<<(io.N + fs2::NC - 1) / fs2::NC, fs2::THREADS, hs, io.stream>>>(a, io.st, slot,
+                                                                          p_override);
+  }
+  auto wk = fs2::wpass<BC, KJ>;
+  const int ws = int(fs2::w_smem(io.K));
+  cudaFuncSetAttribute(wk, cudaFuncAttributeMaxDynamicSharedMemorySize, ws);
+  wk<<<dim3(fs->s2_rc, fs->s2_S), fs2::THREADS, ws, io.stream>>>(a, io.st, slot, p_override,
+                                                                 fs->s2_seg);
+  return cudaGetLastError();
+}
+
 template <int BC>
 static cudaError_t launch_simt(FusedState* fs, const FusedArgs& a, const FusedIO& io, int slot,
                                int p_override) {
-  auto kern = fused_pass_simt<BC>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fs->smem));
-  kern<<<fs->G, ST_THREADS, fs->smem, io.stream>>>(a, io.st, slot, p_override);
-  return cudaGetLastError();
+  if (io.K <= 32) return launch_simt2<BC, 1>(fs, a, io, slot, p_override);
+  return launch_simt2<BC, 2>(fs, a, io, slot, p_override);
 }
 
 template <int FBC, bool KAPPA>
@@ -275,11 +295,14 @@ static int enqueue_pass_and_update(FusedState* fs, const FusedIO& io, int slot, 
   if (io.ev_a) FCK(record_event(io.ev_a, io.stream));
   FCK(launch_pass(fs, a, io, slot, p_override));
   if (io.ev_b) FCK(record_event(io.ev_b, io.stream));
+  const bool s2 = !fs->tc;
+  const int gpart = fs->tc ? fs->tc_grid : fs->s2_S;
+  const int gobj = s2 ? fs->s2_S * fs->s2_rc : gpart;
   fused_reduce<<<int((fk2 + 1 + 255) / 256), 256, 0, io.stream>>>(
-      fs->part, fs->opart, fs->tc ? fs->tc_grid : fs->G, int(fk2), io.K,
+      fs->part, fs->opart, gpart, gobj, int(fk2), io.K,
       fs->tc ? fs->tc_f0 : io.F, fs->tc ? fs->tc_cl : 1, io.comm, io.st, slot, p_override);
   FCK(cudaGetLastError());
-  if (io.launches) *io.launches += 2;
+  if (io.launches) *io.launches += (s2 && a.do_h) ? 3 : 2;
   if (io.nranks > 1) {
     ncclResult_t r = ncclAllReduce(io.comm, io.comm, fk2 + 1, ncclDouble, ncclSum, io.nccl,
                                    io.stream);

@@ -31,6 +31,7 @@ constexpr int THREADS = 256;
 constexpr int TF = 64;        // rows per chunk
 constexpr int NC = 32;        // columns per block / step
 constexpr int TFP = TF + 4;   // row stride of the transposed Z tile
+constexpr int VS = NC + 4;    // row stride of the staged V tile (conflict-free reads)
 
 __host__ __device__ inline int kr4(int K) { return (K + 3) & ~3; }
 // row stride of the row-major factor tiles: >= K rounded to 4, = 4 (mod 8)
@@ -39,16 +40,73 @@ __host__ __device__ inline int kj_of(int K) { return K <= 32 ? 1 : 2; }
 
 __host__ inline size_t h_smem(int K) {
   const int rs = krs(K), ks = 32 * kj_of(K);
-  // Hp [NC][rs] (+32 slack), then Ws [TF][rs], C1s/C2s [TF][ks], Zn/Zd [TF][NC],
-  // which the group sums Red [4][2][ks][NC] alias
-  const size_t tiles = size_t(TF) * rs + 2 * size_t(TF) * ks + 2 * size_t(TF) * NC;
-  const size_t red = size_t(8) * ks * NC;
-  return sizeof(float) * (size_t(NC) * rs + 32 + (tiles > red ? tiles : red));
+  // Hp [NC][rs] (+32 slack); two stage buffers {Ws [TF][rs], C1s/C2s [TF][ks],
+  // Vs [TF][VS]}; Zn/Zd [TF][NC], which the group sums Red [4][2][ks][NC] alias
+  const size_t buf = size_t(TF) * rs + 2 * size_t(TF) * ks + size_t(TF) * VS;
+  const size_t z = 2 * size_t(TF) * NC, red = size_t(8) * ks * NC;
+  return sizeof(float) * (size_t(NC) * rs + 32 + 2 * buf + (z > red ? z : red));
 }
 __host__ inline size_t w_smem(int K) {
   const int rs = krs(K);
-  // Ws [TF][rs], Hs [NC][rs] (+64 slack), ZnT/ZdT [NC][TFP]
-  return sizeof(float) * (size_t(TF) * rs + size_t(NC) * rs + 64 + 2 * size_t(NC) * TFP);
+  // Ws [TF][rs]; two stage buffers {Hs [NC][rs] (+64 slack), Vs [TF][VS]};
+  // ZnT/ZdT [NC][TFP]
+  return sizeof(float) * (size_t(TF) * rs + 2 * (size_t(NC) * rs + 64 + size_t(TF) * VS) +
+                          2 * size_t(NC) * TFP);
+}
+
+// ---- elementwise forms of the SIMT pair ------------------------------------
+// One reciprocal per element (rcp.approx + one Newton step, within an ulp of
+// 1/y) shared by the bases and the objective; the series of the
+// cancellation-free objective forms (fused_common.cuh) in Horner form.
+__device__ __forceinline__ float rcp_nr(float y) {
+  float r;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(y));
+  return fmaf(r, fmaf(-y, r, 1.f), r);
+}
+// u - log1p(u) = sum_{j=2..15} (-1)^j u^j / j
+__device__ __forceinline__ float ser0(float u) {
+  float p = -1.f / 15.f;
+#pragma unroll
+  for (int j = 14; j >= 2; --j) p = fmaf(p, u, ((j & 1) ? -1.f : 1.f) / float(j));
+  return u * u * p;
+}
+// (1+u) log1p(u) - u = sum_{j=2..15} (-1)^j u^j / (j (j-1))
+__device__ __forceinline__ float ser1(float u) {
+  float p = -1.f / 210.f;
+#pragma unroll
+  for (int j = 14; j >= 2; --j) p = fmaf(p, u, ((j & 1) ? -1.f : 1.f) / float(j * (j - 1)));
+  return u * u * p;
+}
+// (Zn, Zd) by the beta rule (updates.py:184-200)
+template <int BC>
+__device__ __forceinline__ void zbases(float x, float y, float beta, float& zn, float& zd) {
+  if (BC == BC_2) { zn = x; zd = y; }
+  else if (BC == BC_1) { zn = x * rcp_nr(y); zd = 1.f; }
+  else if (BC == BC_0) { const float r = rcp_nr(y); zn = x * r * r; zd = r; }
+  else bases32<BC>(x, y, beta, zn, zd);
+}
+// d_beta(x | y) (core.py:89-114, cancellation-free) plus the bases
+template <int BC>
+__device__ __forceinline__ float zdiv(float x, float y, float beta, float& zn, float& zd) {
+  if (BC == BC_2) { zn = x; zd = y; const float d = x - y; return 0.5f * d * d; }
+  if (BC == BC_1) {
+    const float r = rcp_nr(y), q = x * r;
+    zn = q; zd = 1.f;
+    if (x == 0.f) return y;
+    const float u = (x - y) * r;
+    if (fabsf(u) < 0.25f) return y * ser1(u);
+    return x * logf(q) - x + y;
+  }
+  if (BC == BC_0) {
+    const float r = rcp_nr(y);
+    zn = x * r * r; zd = r;
+    const float u = (x - y) * r;
+    if (fabsf(u) < 0.25f) return ser0(u);
+    const float t = x * r;
+    return t - logf(t) - 1.f;
+  }
+  bases32<BC>(x, y, beta, zn, zd);
+  return divergence32<BC>(x, y, beta);
 }
 
 // y[i][j] = sum_k Ws[r_i][k] * Hs[c_j][k], rows r_i = 4 tf + i, columns
@@ -75,6 +133,66 @@ __device__ __forceinline__ void vt_tile(const float* Ws, const float* Hs, int rs
   }
 }
 
+__device__ __forceinline__ void cp4(float* dst, const float* src, bool ok) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src),
+               "r"(ok ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+__device__ __forceinline__ void cp16(float* dst, const float* src, int bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes)
+               : "memory");
+}
+
+// 16-byte row copies of a K-wide row-major block (K % 4 == 0, K <= 64): lane l
+// copies chunk l % q (q = K / 4) of row l / q of each group of 32 / q rows,
+// so the loop has no runtime division.  Rows past `valid` are zero-filled;
+// columns >= K are left untouched (they only feed unused accumulators).
+struct RowMap {
+  int rr, c, rpw;
+  bool on;
+};
+__device__ __forceinline__ RowMap row_map(int K) {
+  const int q = K >> 2, lane = threadIdx.x & 31;
+  RowMap m;
+  m.rpw = 32 / q;
+  m.rr = lane / q;
+  m.c = (lane - m.rr * q) * 4;
+  m.on = m.rr < m.rpw;
+  return m;
+}
+__device__ __forceinline__ void rows_async16(float* dst, const float* __restrict__ src, int rows,
+                                             int valid, int K, int rs, const RowMap& m) {
+  if (!m.on) return;
+  for (int r = (threadIdx.x >> 5) * m.rpw + m.rr; r < rows; r += (THREADS / 32) * m.rpw)
+    cp16(dst + r * rs + m.c, r < valid ? src + (size_t)r * K + m.c : src, r < valid ? 16 : 0);
+}
+
+// async form of load_tile (zero fill through the cp.async source size)
+__device__ __forceinline__ void tile_async(float* dst, const float* __restrict__ src, int rows,
+                                           int valid, int K, int rs, int width) {
+  for (int i = threadIdx.x; i < rows * width; i += THREADS) {
+    const int r = i / width, k = i - r * width;
+    const bool ok = r < valid && k < K;
+    cp4(dst + r * rs + k, ok ? src + (size_t)r * K + k : src, ok);
+  }
+}
+
+// V tile [TF rows x NC columns] at v (row stride ldv) -> dst (row stride VS),
+// 16-byte copies (ldv and the column offset are multiples of 4), partial /
+// zero fill past vf rows and vn columns
+__device__ __forceinline__ void vtile_async(float* dst, const float* __restrict__ v, long long ldv,
+                                            int vf, int vn) {
+  for (int i = threadIdx.x; i < TF * (NC / 4); i += THREADS) {
+    const int r = i / (NC / 4), c = (i - r * (NC / 4)) * 4;
+    const int cols = r < vf ? max(0, min(4, vn - c)) : 0;
+    cp16(dst + r * VS + c, cols > 0 ? v + (size_t)r * ldv + c : v, cols * 4);
+  }
+}
+
 // rows [0, rows) of a row-major K-wide global block -> smem row stride rs,
 // zero-filled to width `width` and past `valid` rows
 __device__ __forceinline__ void load_tile(float* dst, const float* __restrict__ src, int rows,
@@ -94,12 +212,10 @@ hpass(FusedArgs a, const RunState* st, int slot, int p_override) {
   constexpr bool DEN = BC != BC_1;   // beta = 1: den = colsum(C2) (updates.py:133-137)
   const int K = a.K, F = a.F, N = a.N, rs = krs(K), kr = kr4(K);
   float* Hp = reinterpret_cast<float*>(smem_raw);   // [NC][rs]
-  float* Ws = Hp + NC * rs + 32;                    // [TF][rs]
-  float* C1s = Ws + TF * rs;                        // [TF][KS]
-  float* C2s = C1s + TF * KS;                       // [TF][KS]
-  float* Zn = C2s + TF * KS;                        // [TF][NC]
+  float* B0 = Hp + NC * rs + 32;                    // 2 x {Ws, C1s, C2s, Vs}
+  const int bsz = TF * rs + 2 * TF * KS + TF * VS;
+  float* Zn = B0 + 2 * bsz;                         // [TF][NC]
   float* Zd = Zn + TF * NC;
-
   const int par = iter_parity(st, slot, p_override);
   const float* Hprev = a.Hbuf[par ^ 1];
   float* Hnew = a.Hout[par];
@@ -115,28 +231,49 @@ hpass(FusedArgs a, const RunState* st, int slot, int p_override) {
   // meet in Red (aliasing the chunk's tiles) and are folded into fp64 in a
   // fixed order.  Thread tid owns the (k, n) outputs e = tid + 256 m.
   constexpr int NOUT = KS * NC / THREADS;
-  float* Red = Ws;                                  // [4][2][KS][NC] after the sums
+  float* Red = Zn;                                  // [4][2][KS][NC] after the sums
   const int fg = tid >> 6, t = tid & 63;
   const int k4 = (t >> 3) * 4, n4 = (t & 7) * 4;
   double accn[NOUT], accd[NOUT];
 #pragma unroll
   for (int m = 0; m < NOUT; ++m) { accn[m] = 0.0; accd[m] = 0.0; }
 
-  for (int f0 = 0; f0 < F; f0 += TF) {
+  const bool k16 = (K & 3) == 0;
+  const RowMap rmap = row_map(k16 ? K : 4);
+  // stage chunk f0 into buffer b: Wa rows, chi maps, V tile (one cp.async group)
+  auto stage = [&](int f0, int b) {
     const int vf = min(TF, F - f0);
-    __syncthreads();
-    load_tile(Ws, Wa + (size_t)f0 * K, TF, vf, K, rs, kr);
-    load_tile(C1s, a.C1 + (size_t)f0 * K, TF, vf, K, KS, KS);
-    if (DEN) load_tile(C2s, a.C2 + (size_t)f0 * K, TF, vf, K, KS, KS);
+    float* ws = B0 + b * bsz;
+    float* c1 = ws + TF * rs;
+    if (k16) {
+      rows_async16(ws, Wa + (size_t)f0 * K, TF, vf, K, rs, rmap);
+      rows_async16(c1, a.C1 + (size_t)f0 * K, TF, vf, K, KS, rmap);
+      if (DEN) rows_async16(c1 + TF * KS, a.C2 + (size_t)f0 * K, TF, vf, K, KS, rmap);
+    } else {
+      tile_async(ws, Wa + (size_t)f0 * K, TF, vf, K, rs, kr);
+      tile_async(c1, a.C1 + (size_t)f0 * K, TF, vf, K, KS, KS);
+      if (DEN) tile_async(c1 + TF * KS, a.C2 + (size_t)f0 * K, TF, vf, K, KS, KS);
+    }
+    vtile_async(c1 + 2 * TF * KS, a.V + (size_t)f0 * a.ldv + n0, a.ldv, vf, valid_n);
+    cp_commit();
+  };
+  stage(0, 0);
+
+  int buf = 0;
+  for (int f0 = 0; f0 < F; f0 += TF, buf ^= 1) {
+    const int vf = min(TF, F - f0);
+    cp_wait_all();
+    __syncthreads();                       // chunk f0 visible; buffer buf^1 free
+    if (f0 + TF < F) stage(f0 + TF, buf ^ 1);
+    const float* Ws = B0 + buf * bsz;
+    const float* C1s = Ws + TF * rs;
+    const float* C2s = C1s + TF * KS;
+    const float* Vs = C2s + TF * KS;
     float x[4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int f = tf * 4 + i, n = tn + 16 * j;
-        x[i][j] = (f < vf && n < valid_n) ? a.V[(size_t)(f0 + f) * a.ldv + n0 + n] : 0.f;
-      }
-    __syncthreads();
+      for (int j = 0; j < 2; ++j) x[i][j] = Vs[(tf * 4 + i) * VS + tn + 16 * j];
     float y[4][2];
     vt_tile(Ws, Hp, rs, kr, tf, tn, y);
 #pragma unroll
@@ -145,7 +282,7 @@ hpass(FusedArgs a, const RunState* st, int slot, int p_override) {
       for (int j = 0; j < 2; ++j) {
         const int f = tf * 4 + i, n = tn + 16 * j;
         float zn = 0.f, zd = 0.f;
-        if (f < vf && n < valid_n) bases32<BC>(x[i][j], y[i][j] + kappa, beta, zn, zd);
+        if (f < vf && n < valid_n) zbases<BC>(x[i][j], y[i][j] + kappa, beta, zn, zd);
         Zn[f * NC + n] = zn;
         if (DEN) Zd[f * NC + n] = zd;
       }
@@ -187,7 +324,7 @@ hpass(FusedArgs a, const RunState* st, int slot, int p_override) {
         }
       }
     }
-    __syncthreads();   // tiles dead: Red aliases them
+    __syncthreads();   // Zn/Zd dead: Red aliases them
     float* rn = Red + (size_t)fg * 2 * KS * NC;
     float* rd = rn + KS * NC;
 #pragma unroll
@@ -235,8 +372,9 @@ wpass(FusedArgs a, const RunState* st, int slot, int p_override, int seg_cols) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int K = a.K, F = a.F, N = a.N, rs = krs(K), kr = kr4(K);
   float* Ws = reinterpret_cast<float*>(smem_raw);   // [TF][rs]
-  float* Hs = Ws + TF * rs;                         // [NC][rs] (+64 slack for the k-pair reads)
-  float* ZnT = Hs + NC * rs + 64;                   // [NC][TFP]
+  float* B0 = Ws + TF * rs;                         // 2 x {Hs [NC][rs] (+64), Vs [TF][VS]}
+  const int bsz = NC * rs + 64 + TF * VS;
+  float* ZnT = B0 + 2 * bsz;                        // [NC][TFP]
   float* ZdT = ZnT + NC * TFP;
   __shared__ double red[THREADS / 32];
 
@@ -249,7 +387,19 @@ wpass(FusedArgs a, const RunState* st, int slot, int p_override, int seg_cols) {
   const int f0 = blockIdx.x * TF, vf = min(TF, F - f0);
   const int nbeg = blockIdx.y * seg_cols, nend = min(N, nbeg + seg_cols);
 
-  load_tile(Ws, Wt + (size_t)f0 * K, TF, vf, K, rs, kr);
+  const bool k16 = (K & 3) == 0;
+  const RowMap rmap = row_map(k16 ? K : 4);
+  // stage step n0 into buffer b: H~_p rows and the V tile (one cp.async group)
+  auto stage = [&](int n0, int b) {
+    const int vn = min(NC, nend - n0);
+    float* hs = B0 + b * bsz;
+    if (k16) rows_async16(hs, Hc + (size_t)n0 * K, NC, vn, K, rs, rmap);
+    else tile_async(hs, Hc + (size_t)n0 * K, NC, vn, K, rs, kr);
+    vtile_async(hs + NC * rs + 64, a.V + (size_t)f0 * a.ldv + n0, a.ldv, vf, vn);
+    cp_commit();
+  };
+  tile_async(Ws, Wt + (size_t)f0 * K, TF, vf, K, rs, kr);
+  if (nbeg < nend) stage(nbeg, 0);
 
   double pn[KJ][4][2], pd[KJ][4][2];
 #pragma unroll
@@ -258,19 +408,19 @@ wpass(FusedArgs a, const RunState* st, int slot, int p_override, int seg_cols) {
     for (int i = 0; i < 4; ++i) { pn[j][i][0] = pn[j][i][1] = 0.0; pd[j][i][0] = pd[j][i][1] = 0.0; }
   double obj = 0.0;
 
-  for (int n0 = nbeg; n0 < nend; n0 += NC) {
+  int buf = 0;
+  for (int n0 = nbeg; n0 < nend; n0 += NC, buf ^= 1) {
     const int valid_n = min(NC, nend - n0);
-    __syncthreads();
-    load_tile(Hs, Hc + (size_t)n0 * K, NC, valid_n, K, rs, kr);
+    cp_wait_all();
+    __syncthreads();                       // step n0 visible; buffer buf^1 and Z free
+    if (n0 + NC < nend) stage(n0 + NC, buf ^ 1);
+    const float* Hs = B0 + buf * bsz;
+    const float* Vs = Hs + NC * rs + 64;
     float x[4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int f = tf * 4 + i, n = tn + 16 * j;
-        x[i][j] = (f < vf && n < valid_n) ? a.V[(size_t)(f0 + f) * a.ldv + n0 + n] : 0.f;
-      }
-    __syncthreads();
+      for (int j = 0; j < 2; ++j) x[i][j] = Vs[(tf * 4 + i) * VS + tn + 16 * j];
     float y[4][2];
     vt_tile(Ws, Hs, rs, kr, tf, tn, y);
     float zn[4][2], zd[4][2], ob = 0.f;
@@ -281,9 +431,7 @@ wpass(FusedArgs a, const RunState* st, int slot, int p_override, int seg_cols) {
         zn[i][j] = 0.f; zd[i][j] = 0.f;
         const int f = tf * 4 + i, n = tn + 16 * j;
         if (f < vf && n < valid_n) {
-          const float yy = y[i][j] + kappa;
-          ob += divergence32<BC>(x[i][j], yy, beta);
-          bases32<BC>(x[i][j], yy, beta, zn[i][j], zd[i][j]);
+          ob += zdiv<BC>(x[i][j], y[i][j] + kappa, beta, zn[i][j], zd[i][j]);
         }
       }
     obj += double(ob);
@@ -327,6 +475,7 @@ wpass(FusedArgs a, const RunState* st, int slot, int p_override, int seg_cols) {
           pd[j][i][v] += double(sd[j][i][v]);
         }
   }
+  cp_wait_all();
   // this segment's slab: rows [f0, f0+vf) of part[seg][2][F][K]
   double* slab = a.part + (size_t)blockIdx.y * 2 * F * K;
 #pragma unroll

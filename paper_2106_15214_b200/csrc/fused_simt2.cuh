@@ -232,7 +232,11 @@ hpass(FusedArgs a, const RunState* st, int slot, int p_override) {
   // fixed order.  Thread tid owns the (k, n) outputs e = tid + 256 m.
   constexpr int NOUT = KS * NC / THREADS;
   float* Red = Zn;                                  // [4][2][KS][NC] after the sums
-  const int fg = tid >> 6, t = tid & 63;
+  // K <= 32: only ceil(K/4) k-quads per group are live, so whole warps of
+  // the 4 x 8 x nk4 layout sit the sums out instead of computing padding
+  const int nk4 = KJ == 1 ? (K + 3) >> 2 : 8;
+  const bool hact = tid < 32 * nk4;
+  const int fg = tid / (8 * nk4), t = tid - fg * 8 * nk4;
   const int k4 = (t >> 3) * 4, n4 = (t & 7) * 4;
   double accn[NOUT], accd[NOUT];
 #pragma unroll
@@ -295,7 +299,7 @@ hpass(FusedArgs a, const RunState* st, int slot, int p_override) {
       for (int u = 0; u < 4; ++u)
 #pragma unroll
         for (int v = 0; v < 4; ++v) { sn[j][u][v] = 0.f; sd[j][u][v] = 0.f; }
-    const int fe = min(16, vf - fg * 16);
+    const int fe = hact ? min(16, vf - fg * 16) : 0;
 #pragma unroll 2
     for (int ff = 0; ff < fe; ++ff) {
       const int f = fg * 16 + ff;
@@ -328,7 +332,7 @@ hpass(FusedArgs a, const RunState* st, int slot, int p_override) {
     float* rn = Red + (size_t)fg * 2 * KS * NC;
     float* rd = rn + KS * NC;
 #pragma unroll
-    for (int j = 0; j < KJ; ++j)
+    for (int j = 0; j < KJ && hact; ++j)
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int k = k4 + 32 * j + u;
@@ -383,7 +387,11 @@ wpass(FusedArgs a, const RunState* st, int slot, int p_override, int seg_cols) {
   const float* Hc = a.do_h ? a.Hout[par] : a.Hbuf[par];     // H~_p
   const float kappa = float(a.sc.kappa), beta = float(a.sc.beta);
   const int tid = threadIdx.x, tn = tid & 15, tf = tid >> 4;
-  const int cf = (tid >> 4) * 4, ck = (tid & 15) * 2;   // W-sum tile: 4 rows x k pair
+  // W-sum tile: 4 rows x k pair; K <= 32: ceil(K/2) live pairs, the other
+  // warps sit the sums out
+  const int kp2 = KJ == 1 ? (K + 1) >> 1 : 16;
+  const bool cact = tid < 16 * kp2;
+  const int cf = (tid / kp2) * 4, ck = (tid % kp2) * 2;
   const int f0 = blockIdx.x * TF, vf = min(TF, F - f0);
   const int nbeg = blockIdx.y * seg_cols, nend = min(N, nbeg + seg_cols);
 
@@ -450,8 +458,9 @@ wpass(FusedArgs a, const RunState* st, int slot, int p_override, int seg_cols) {
     for (int j = 0; j < KJ; ++j)
 #pragma unroll
       for (int i = 0; i < 4; ++i) { sn[j][i][0] = sn[j][i][1] = 0.f; sd[j][i][0] = sd[j][i][1] = 0.f; }
+    const int ne = cact ? valid_n : 0;
 #pragma unroll 4
-    for (int n = 0; n < valid_n; ++n) {
+    for (int n = 0; n < ne; ++n) {
       const float4 z = *reinterpret_cast<const float4*>(ZnT + n * TFP + cf);
       const float4 d = *reinterpret_cast<const float4*>(ZdT + n * TFP + cf);
       const float zz[4] = {z.x, z.y, z.z, z.w}, dd[4] = {d.x, d.y, d.z, d.w};
@@ -485,7 +494,7 @@ wpass(FusedArgs a, const RunState* st, int slot, int p_override, int seg_cols) {
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int f = cf + i, k = ck + 32 * j + v;
-        if (f < vf && k < K) {
+        if (cact && f < vf && k < K) {
           const size_t idx = (size_t)(f0 + f) * K + k;
           slab[idx] = pn[j][i][v];
           slab[(size_t)F * K + idx] = pd[j][i][v];

@@ -23,8 +23,17 @@ static __global__ void fused_reduce(const double* __restrict__ part, const doubl
   if (i < FK2) {
     const int f = (i % (FK2 / 2)) / K;
     const int r = (cl > 1 && f >= split) ? 1 : 0;
+    // loads batched 8 at a time, summed in slab order
     double s = 0.0;
-    for (int g = r; g < G; g += cl) s += part[(size_t)g * FK2 + i];
+    int g = r;
+    for (; g + 7 * cl < G; g += 8 * cl) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = part[(size_t)(g + u * cl) * FK2 + i];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; g < G; g += cl) s += part[(size_t)g * FK2 + i];
     comm[i] = s;
   } else if (i == FK2) {
     double s = 0.0;
@@ -39,7 +48,7 @@ static __global__ void fused_reduce(const double* __restrict__ part, const doubl
 //   C1 = chi1(W_{p+1}, W~_p), C2 = chi2(...) (JMM) or W_{p+1} (BMM)
 struct WPair { float* w[2]; };
 
-static __global__ void fused_update(const double* __restrict__ comm, int F, int K,
+static __global__ void __launch_bounds__(1024) fused_update(const double* __restrict__ comm, int F, int K,
                              WPair Wt2, float* Wn, float* C1, float* C2, double* norms,
                              double* csum2,
                              int algorithm, int den_ones, Scalars sc, const RunState* st, int slot,

@@ -100,6 +100,9 @@ static cudaLaunchConfig_t tc_config(const FusedState* fs, cudaStream_t stream,
     }                                                                       \
   } while (0)
 
+// one thread per row of W for F <= 1024 (no serial latency chain per column)
+constexpr int FU_THREADS = 1024;
+
 bool fused_supported(int dtype, int F, int K, int algorithm, int L, int Lw, int Lh, double beta) {
   (void)F; (void)beta;
   if (dtype != BNMF_FP32) return false;
@@ -317,7 +320,7 @@ static int enqueue_pass_and_update(FusedState* fs, const FusedIO& io, int slot, 
   }
   WPair wp;
   wp.w[0] = fs->W2[0]; wp.w[1] = fs->W2[1];
-  fused_update<<<io.K, 256, 0, io.stream>>>(io.comm, io.F, io.K, wp, fs->Wn, fs->C1, fs->C2,
+  fused_update<<<io.K, FU_THREADS, 0, io.stream>>>(io.comm, io.F, io.K, wp, fs->Wn, fs->C1, fs->C2,
                                             fs->norms, fs->csum2, io.algorithm, a.den_ones, io.sc,
                                             io.st, slot, p_override);
   FCK(cudaGetLastError());

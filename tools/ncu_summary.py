@@ -46,6 +46,8 @@ def main():
     isrc, ie, iw = sh.index("Source"), sh.index("Instructions Executed"), sh.index("Warp Stall Sampling (All Samples)")
     ops, samp = collections.Counter(), collections.Counter()
     for r in data:
+        if len(r) <= max(isrc, ie, iw) or r[ie] == "Instructions Executed":
+            continue   # header row of the next kernel in a multi-kernel report
         m = re.match(r"\s*(@!?U?P\w+\s+)?([A-Z0-9_]+)", r[isrc])
         if m:
             ops[m.group(2)] += float(r[ie] or 0)

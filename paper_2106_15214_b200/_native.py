@@ -26,6 +26,9 @@ class NativeUnavailable(RuntimeError):
     """libbnmf.so is not built or cannot run here (no CUDA device)."""
 
 
+BNMF_E_ARG = -1   # include/bnmf.h
+
+
 class NativeError(RuntimeError):
     """A libbnmf call returned an error code."""
 
@@ -203,7 +206,14 @@ class Context:
         if w.shape[0] != self.F or h.shape[1] != self.N or w.shape[1] != h.shape[0]:
             raise ValueError("factor shapes do not match the data")
         self.K = w.shape[1]
-        self._check(self.lib.bnmf_set_factors(self.h, _ptr(w), _ptr(h), self.K, 0))
+        rc = self.lib.bnmf_set_factors(self.h, _ptr(w), _ptr(h), self.K, 0)
+        if rc == BNMF_E_ARG:
+            # the FactorPair checks, made on the device copy (core.py: FactorPair.__post_init__)
+            msg = self.lib.bnmf_last_error(self.h)
+            msg = msg.decode() if msg else ""
+            if msg.startswith("factor entries"):
+                raise ValueError(msg)
+        self._check(rc)
 
     # -- running -----------------------------------------------------------
 

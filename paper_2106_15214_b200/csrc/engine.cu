@@ -21,6 +21,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <type_traits>
 #include <vector>
 
@@ -52,6 +53,27 @@ static thread_local std::string g_err;
 
 namespace bnmf {
 
+// Host memcpy split over up to 8 threads (large pageable result / init arrays:
+// the copy and its first-touch page faults are spread over cores).
+static void par_memcpy(void* dst, const void* src, size_t bytes) {
+  const size_t per_min = size_t(4) << 20;
+  const int nt = int(std::min<size_t>(8, std::max<size_t>(1, bytes / per_min)));
+  if (nt <= 1) {
+    memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t per = (bytes + nt - 1) / nt;
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) {
+    const size_t a = size_t(t) * per;
+    if (a >= bytes) break;
+    const size_t n = std::min(per, bytes - a);
+    th.emplace_back([=] { memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, n); });
+  }
+  memcpy(dst, src, std::min(per, bytes));
+  for (auto& t : th) t.join();
+}
+
 int EngineBase::fail(int code, const std::string& msg) {
   err = msg;
   g_err = msg;
@@ -81,6 +103,11 @@ struct Engine : EngineBase {
   RunState* st_host = nullptr;
   void* staging = nullptr;
   size_t staging_bytes = 0;
+  // pinned bounce buffers (2 x HB_CHUNK) for pageable host <-> device copies
+  static constexpr size_t HB_CHUNK = size_t(32) << 20;
+  char* hbounce = nullptr;
+  cudaEvent_t hb_ev[2] = {nullptr, nullptr};
+  double* fstats = nullptr;   // min / max / sum / non-finite of the uploaded factors
   // schedule
   int S = 1, seg_cols = 32;
   int n_hblocks = 1, n_oblocks = 1;
@@ -122,6 +149,9 @@ struct Engine : EngineBase {
     if (st) cudaFree(st);
     if (st_host) cudaFreeHost(st_host);
     if (staging) cudaFree(staging);
+    if (hbounce) cudaFreeHost(hbounce);
+    for (cudaEvent_t e : hb_ev) if (e) cudaEventDestroy(e);
+    if (fstats) cudaFree(fstats);
     if (stats_part) cudaFree(stats_part);
     if (stats_acc) cudaFree(stats_acc);
     if (fused) fused_destroy(fused);
@@ -145,18 +175,79 @@ struct Engine : EngineBase {
     return 0;
   }
 
+  int ensure_bounce() {
+    if (hbounce) return 0;
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&hbounce), 2 * HB_CHUNK, cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&hb_ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&hb_ev[1], cudaEventDisableTiming));
+    return 0;
+  }
+
+  // pageable host -> device through the pinned bounce buffers: the host copy
+  // of chunk c overlaps the DMA of chunk c-1 (a direct pageable copy runs at
+  // a fraction of the link rate)
+  int h2d_bounce(void* dst, const void* src, size_t bytes) {
+    if (bytes < 2 * HB_CHUNK) {
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
+      CK(cudaStreamSynchronize(stream));
+      return 0;
+    }
+    if (int rc = ensure_bounce()) return rc;
+    const size_t nch = (bytes + HB_CHUNK - 1) / HB_CHUNK;
+    for (size_t c = 0; c < nch; ++c) {
+      const int b = int(c & 1);
+      const size_t off = c * HB_CHUNK, n = std::min(HB_CHUNK, bytes - off);
+      if (c >= 2) CK(cudaEventSynchronize(hb_ev[b]));
+      par_memcpy(hbounce + b * HB_CHUNK, static_cast<const char*>(src) + off, n);
+      CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, hbounce + b * HB_CHUNK, n,
+                         cudaMemcpyHostToDevice, stream));
+      CK(cudaEventRecord(hb_ev[b], stream));
+    }
+    CK(cudaStreamSynchronize(stream));
+    return 0;
+  }
+
+  // device -> pageable host, the mirror image: the DMA of chunk c+1 overlaps
+  // the host copy of chunk c
+  int d2h_bounce(void* dst, const void* src, size_t bytes) {
+    if (bytes < 2 * HB_CHUNK) {
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      return 0;
+    }
+    if (int rc = ensure_bounce()) return rc;
+    const size_t nch = (bytes + HB_CHUNK - 1) / HB_CHUNK;
+    auto issue = [&](size_t c) -> cudaError_t {
+      const size_t off = c * HB_CHUNK, n = std::min(HB_CHUNK, bytes - off);
+      cudaError_t e = cudaMemcpyAsync(hbounce + (c & 1) * HB_CHUNK,
+                                      static_cast<const char*>(src) + off, n,
+                                      cudaMemcpyDeviceToHost, stream);
+      return e != cudaSuccess ? e : cudaEventRecord(hb_ev[c & 1], stream);
+    };
+    CK(issue(0));
+    for (size_t c = 0; c < nch; ++c) {
+      if (c + 1 < nch) CK(issue(c + 1));
+      CK(cudaEventSynchronize(hb_ev[c & 1]));
+      const size_t off = c * HB_CHUNK, n = std::min(HB_CHUNK, bytes - off);
+      par_memcpy(static_cast<char*>(dst) + off, hbounce + (c & 1) * HB_CHUNK, n);
+    }
+    return 0;
+  }
+
   // statistics of a rows x cols source block, accumulated into stats_acc
   double* stats_part = nullptr;
   double* stats_acc = nullptr;
   int64_t stats_count = 0;
   template <typename S_>
   int stats_of(const S_* src, size_t lds, int rows, size_t cols, bool first) {
-    if (!stats_part) {
-      CK(cudaMalloc(&stats_part, STATS_BLOCKS * 4 * sizeof(double)));
-      CK(cudaMalloc(&stats_acc, 4 * sizeof(double)));
-    }
+    if (!stats_acc) CK(cudaMalloc(&stats_acc, 4 * sizeof(double)));
+    return stats_into(src, lds, rows, cols, first, stats_acc);
+  }
+  template <typename S_>
+  int stats_into(const S_* src, size_t lds, int rows, size_t cols, bool first, double* acc) {
+    if (!stats_part) CK(cudaMalloc(&stats_part, STATS_BLOCKS * 4 * sizeof(double)));
     stats_partial<S_><<<STATS_BLOCKS, 256, 0, stream>>>(src, lds, rows, cols, stats_part);
-    stats_final<<<1, 32, 0, stream>>>(stats_part, STATS_BLOCKS, stats_acc, first ? 1 : 0);
+    stats_final<<<1, 32, 0, stream>>>(stats_part, STATS_BLOCKS, acc, first ? 1 : 0);
     CK(cudaGetLastError());
     return 0;
   }
@@ -272,23 +363,32 @@ struct Engine : EngineBase {
     size_t fk = size_t(F) * K, nk = size_t(N) * K;
     if (int rc = ensure_staging(std::max(fk, nk) * sizeof(double))) return rc;
     double* stg = reinterpret_cast<double*>(staging);
+    if (!fstats) CK(cudaMalloc(&fstats, 4 * sizeof(double)));
     const double* wsrc = w;
     if (!on_dev) {
-      CK(cudaMemcpyAsync(stg, w, fk * sizeof(double), cudaMemcpyHostToDevice, stream));
+      if (int rc = h2d_bounce(stg, w, fk * sizeof(double))) return rc;
       wsrc = stg;
     }
+    // the FactorPair checks (core.py:__post_init__ of the reference's
+    // FactorPair) on the device copy, so large inits need no host scan
+    if (int rc = stats_into(wsrc, fk, 1, fk, true, fstats)) return rc;
     from_double<T><<<grid_for(fk), 256, 0, stream>>>(wsrc, fk, Wt);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(stream));
     const double* hsrc = h;
     if (!on_dev) {
-      CK(cudaMemcpyAsync(stg, h, nk * sizeof(double), cudaMemcpyHostToDevice, stream));
+      if (int rc = h2d_bounce(stg, h, nk * sizeof(double))) return rc;
       hsrc = stg;
     }
+    if (int rc = stats_into(hsrc, nk, 1, nk, false, fstats)) return rc;
     transpose_in<T><<<grid_for(nk), 256, 0, stream>>>(hsrc, K, size_t(N), Ht);
     CK(cudaGetLastError());
+    double fs[4];
+    CK(cudaMemcpyAsync(fs, fstats, sizeof(fs), cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
     begun = false;
+    if (fs[3] > 0.0) return fail(BNMF_E_ARG, "factor entries must be finite");
+    if (fs[0] <= 0.0) return fail(BNMF_E_ARG, "factor entries must be strictly positive");
     return 0;
   }
 
@@ -303,13 +403,10 @@ struct Engine : EngineBase {
     }
     to_double<T><<<grid_for(fk), 256, 0, stream>>>(Wt, fk, stg);
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(w, stg, fk * sizeof(double), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
+    if (int rc = d2h_bounce(w, stg, fk * sizeof(double))) return rc;
     transpose_out<T><<<grid_for(nk), 256, 0, stream>>>(Ht, K, size_t(N), stg);
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(h, stg, nk * sizeof(double), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    return 0;
+    return d2h_bounce(h, stg, nk * sizeof(double));
   }
 
   // ------------------------------------------------------------------------

@@ -289,11 +289,23 @@ def _count_ops(counter, config, iterations):
     counter.objective_products += iterations
 
 
-def _resolve_init(init, F, N, K, seed):
+def _resolve_init(init, F, N, K, seed, device_checked=False):
+    """FactorPair of the init.  ``device_checked``: an array init of >= 2^24
+    entries skips the host finiteness / positivity scans, which
+    Context.set_factors then makes on the device copy with the same messages
+    (core.py FactorPair.__post_init__)."""
     if init is None:
         return init_factors(F, N, K, seed)
     if isinstance(init, FactorPair):
         pair = init
+    elif device_checked and np.asarray(init[1]).size >= _DEVICE_CHECK_MIN:
+        w = np.asarray(init[0], dtype=float)
+        h = np.asarray(init[1], dtype=float)
+        if w.ndim != 2 or h.ndim != 2:
+            raise ValueError("factors must be 2-D matrices")
+        if w.shape[1] != h.shape[0]:
+            raise ValueError(f"inner dimensions disagree: w is {w.shape}, h is {h.shape}")
+        pair = _unchecked_pair(w, h)
     else:
         pair = FactorPair(*init)
     if pair.w.shape != (F, K) or pair.h.shape != (K, N):
@@ -364,7 +376,7 @@ def _run(data, config, counter, algorithm, *, dtype="fp64", init=None, device=No
         if data is None:
             data, F, N = _upload_checked(ctx, values, config)
             n_global = N
-            pair = _resolve_init(init, F, N, config.rank, config.seed)
+            pair = _resolve_init(init, F, N, config.rank, config.seed, device_checked=True)
         else:
             ctx.set_dense(data.values, data.kappa)
         ctx.set_factors(pair.w, pair.h)

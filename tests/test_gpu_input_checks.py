@@ -68,3 +68,29 @@ def test_auto_kappa_matches_host_rule():
     a = np.array([t.objective for t in dev.trace])
     b = np.array([t.objective for t in host.trace])
     assert np.allclose(a, b, rtol=1e-6)
+
+
+@pytest.mark.parametrize("where,bad,msg", [
+    ("h", np.nan, "factor entries must be finite"),
+    ("w", np.inf, "factor entries must be finite"),
+    ("h", 0.0, "factor entries must be strictly positive"),
+    ("w", -2.0, "factor entries must be strictly positive"),
+])
+def test_large_init_checked_on_device(where, bad, msg):
+    """An injected init of >= 2^24 entries is validated on its device copy
+    (Context.set_factors), with the reference FactorPair's messages."""
+    Fi, Ni, K = 64, 1 << 18, 64
+    assert K * Ni >= solver._DEVICE_CHECK_MIN
+    rng = np.random.default_rng(2)
+    v = (rng.random((Fi, Ni), dtype=np.float32) + 0.5).astype(np.float32)
+    w0 = rng.random((Fi, K)) + 0.1
+    h0 = rng.random((K, Ni)) + 0.1
+    cfg = bn.SolverConfig(beta=1.0, rank=K, algorithm="jmm", max_outer_iters=2, tol=1e-300)
+    res = bn.fit(v, cfg, init=(w0, h0), dtype="fp32", kkt=False)
+    assert res.iterations == 2
+    (w0 if where == "w" else h0)[5, 7] = bad
+    with pytest.raises(ValueError, match=msg):
+        bn.fit(v, cfg, init=(w0, h0), dtype="fp32", kkt=False)
+    # the host path (small data) raises the same message
+    with pytest.raises(ValueError, match=msg):
+        bn.fit(v[:, :64], cfg, init=(w0, h0[:, :64]), dtype="fp32", kkt=False)

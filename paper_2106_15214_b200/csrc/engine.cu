@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -273,19 +274,25 @@ struct Engine : EngineBase {
     int rpc = int(std::max<size_t>(1, chunk_bytes / (cols * sizeof(S_))));
     rpc = std::min(rpc, rows);
     if (int rc = ensure_staging(size_t(rpc) * cols * sizeof(S_))) return rc;
+    // one stream orders copy(c+1) after convert(c), so the staging buffer is
+    // reused without host syncs and the link stays busy; contiguous rows
+    // (lds == cols) go as one linear copy
     for (int r0 = 0; r0 < rows; r0 += rpc) {
       int nr = std::min(rpc, rows - r0);
-      CK(cudaMemcpy2DAsync(staging, cols * sizeof(S_),
-                           reinterpret_cast<const S_*>(src) + size_t(r0) * lds,
-                           lds * sizeof(S_), cols * sizeof(S_), nr,
-                           cudaMemcpyHostToDevice, stream));
+      const S_* s0 = reinterpret_cast<const S_*>(src) + size_t(r0) * lds;
+      if (lds == cols)
+        CK(cudaMemcpyAsync(staging, s0, size_t(nr) * cols * sizeof(S_), cudaMemcpyHostToDevice,
+                           stream));
+      else
+        CK(cudaMemcpy2DAsync(staging, cols * sizeof(S_), s0, lds * sizeof(S_),
+                             cols * sizeof(S_), nr, cudaMemcpyHostToDevice, stream));
       if (int rc = stats_of(reinterpret_cast<const S_*>(staging), cols, nr, cols, r0 == 0)) return rc;
       convert_rows<S_, T><<<grid_for(size_t(nr) * cols), 256, 0, stream>>>(
           reinterpret_cast<const S_*>(staging), cols, V + size_t(r0) * ldv, ldv, nr, cols,
           kappa);
       CK(cudaGetLastError());
-      CK(cudaStreamSynchronize(stream));
     }
+    CK(cudaStreamSynchronize(stream));
     return 0;
   }
 

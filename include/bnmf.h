@@ -101,7 +101,10 @@ int bnmf_set_csr(bnmf_ctx* ctx, const int64_t* indptr, const int32_t* indices,
                  const int32_t* perm, int64_t F, int64_t N, int64_t nnz, int src_on_device);
 
 /* Factors: W (F x K) and the local H block (K x N), fp64 row-major host or
- * device memory (init_factors, solver.py:137-153, or an injected init). */
+ * device memory (init_factors, solver.py:137-153, or an injected init).
+ * Applies the reference FactorPair checks (core.py FactorPair.__post_init__)
+ * to the device copy: BNMF_E_ARG with "factor entries must be finite" or
+ * "factor entries must be strictly positive" (the reference's messages). */
 int bnmf_set_factors(bnmf_ctx* ctx, const double* w, const double* h, int64_t K,
                      int src_on_device);
 

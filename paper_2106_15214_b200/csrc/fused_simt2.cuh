@@ -57,7 +57,10 @@ __host__ inline size_t w_smem(int K) {
 // ---- elementwise forms of the SIMT pair ------------------------------------
 // One reciprocal per element (rcp.approx + one Newton step, within an ulp of
 // 1/y) shared by the bases and the objective; the series of the
-// cancellation-free objective forms (fused_common.cuh) in Horner form.
+// cancellation-free objective forms (fused_common.cuh) in Horner form.  The
+// log of the far branch (|t - 1| >= 1/4, so |log t| >= 0.22) is MUFU.LG2
+// based (__logf: absolute error ~2^-21 near 1, relative ~2 ulp elsewhere),
+// i.e. <= ~1e-5 relative on such an element.
 __device__ __forceinline__ float rcp_nr(float y) {
   float r;
   asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(y));
@@ -95,7 +98,7 @@ __device__ __forceinline__ float zdiv(float x, float y, float beta, float& zn, f
     if (x == 0.f) return y;
     const float u = (x - y) * r;
     if (fabsf(u) < 0.25f) return y * ser1(u);
-    return x * logf(q) - x + y;
+    return x * __logf(q) - x + y;
   }
   if (BC == BC_0) {
     const float r = rcp_nr(y);
@@ -103,7 +106,7 @@ __device__ __forceinline__ float zdiv(float x, float y, float beta, float& zn, f
     const float u = (x - y) * r;
     if (fabsf(u) < 0.25f) return ser0(u);
     const float t = x * r;
-    return t - logf(t) - 1.f;
+    return t - __logf(t) - 1.f;
   }
   bases32<BC>(x, y, beta, zn, zd);
   return divergence32<BC>(x, y, beta);

@@ -194,8 +194,13 @@ __global__ void __launch_bounds__(256) stats_partial(const S* __restrict__ src, 
   const size_t count = (size_t)rows * cols;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
        i += (size_t)gridDim.x * blockDim.x) {
-    const size_t r = i / cols, c = i - r * cols;
-    const double v = double(src[r * lds + c]);
+    // contiguous rows (lds == cols, e.g. the factor checks): no 64-bit divide
+    size_t j = i;
+    if (lds != cols) {
+      const size_t r = i / cols;
+      j = r * lds + (i - r * cols);
+    }
+    const double v = double(src[j]);
     if (isfinite(v)) {
       mn = fmin(mn, v);
       mx = fmax(mx, v);

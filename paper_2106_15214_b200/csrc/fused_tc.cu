@@ -111,6 +111,34 @@ bool fused_supported(int dtype, int F, int K, int algorithm, int L, int Lw, int 
   return Lw == 1 && Lh == 1;
 }
 
+template <int BC, int KJ>
+static int wpass_occ(int K) {
+  auto k = fs2::wpass<BC, KJ>;
+  const int sm = int(fs2::w_smem(K));
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, fs2::THREADS, sm) != cudaSuccess) {
+    cudaGetLastError();
+    n = 2;
+  }
+  return std::max(1, n);
+}
+
+template <int KJ>
+static int wpass_occ_bc(int bc, int K) {
+  switch (bc) {
+    case BC_0: return wpass_occ<BC_0, KJ>(K);
+    case BC_1: return wpass_occ<BC_1, KJ>(K);
+    case BC_2: return wpass_occ<BC_2, KJ>(K);
+    default: return wpass_occ<BC_GEN, KJ>(K);
+  }
+}
+
+// resident wpass CTAs per SM for this beta class and rank
+static int wpass_occupancy(int bc, int K) {
+  return K <= 32 ? wpass_occ_bc<1>(bc, K) : wpass_occ_bc<2>(bc, K);
+}
+
 int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
   FusedState* fs = new FusedState;
   *out = fs;
@@ -129,10 +157,13 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   {
-    // wpass: about two CTAs per SM, column segments in whole 32-column steps
+    // wpass: one wave of CTAs (row chunks x column segments <= resident
+    // slots, rounded down: a partial second wave would double the tail), the
+    // segments in whole 32-column steps
     const int ncb = (io.N + fs2::NC - 1) / fs2::NC;
     fs->s2_rc = (io.F + fs2::TF - 1) / fs2::TF;
-    int S = std::max(1, std::min(ncb, (2 * nsm + fs->s2_rc - 1) / fs->s2_rc));
+    const int slots = nsm * wpass_occupancy(beta_class(io.sc.beta), io.K);
+    int S = std::max(1, std::min(ncb, slots / fs->s2_rc));
     const int steps = (ncb + S - 1) / S;
     fs->s2_seg = steps * fs2::NC;
     fs->s2_S = (io.N + fs->s2_seg - 1) / fs->s2_seg;

@@ -34,6 +34,6 @@ for r in rows:
 tot = sum(a[0] for a in agg) or 1
 toti = sum(a[1] for a in agg) or 1
 print(f"total samples {tot}, warp-instructions {toti}")
-for s, i, loc, src, st in sorted(agg, reverse=True, key=(lambda a: a[1]) if byinst else None)[:top]:
+for s, i, loc, src, st in sorted(agg, reverse=True, key=(lambda a: a[1]) if byinst else (lambda a: a[0]))[:top]:
     top3 = ", ".join(f"{k} {v}" for k, v in sorted(st.items(), key=lambda x: -x[1])[:3])
     print(f"{100*s/tot:5.1f}% inst {100*i/toti:5.1f}%  {loc:28s} {src:70s} [{top3}]")

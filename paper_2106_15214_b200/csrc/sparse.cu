@@ -184,12 +184,27 @@ __global__ void __launch_bounds__(SP_THREADS) sp_colstats(SpArgs a, const RunSta
   const int KL = a.KL, RP = SP_THREADS / KL;
   const int k = threadIdx.x % KL, r = threadIdx.x / KL;
   double cs = 0.0, sq = 0.0;
-  if (k < a.K && r < RP)
-    for (int f = blockIdx.x * RP + r; f < a.F; f += gridDim.x * RP) {
+  if (k < a.K && r < RP) {
+    // 4 rows' loads in flight per step, added in row order
+    const int stride = gridDim.x * RP;
+    int f = blockIdx.x * RP + r;
+    for (; f + 3 * stride < a.F; f += 4 * stride) {
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = a.Wp[size_t(f + u * stride) * KL + k];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double w = double(v[u]);
+        cs += w;
+        sq += w * w;
+      }
+    }
+    for (; f < a.F; f += stride) {
       const double w = double(a.Wp[size_t(f) * KL + k]);
       cs += w;
       sq += w * w;
     }
+  }
   __shared__ double red[2][SP_THREADS];
   red[0][threadIdx.x] = cs;
   red[1][threadIdx.x] = sq;
@@ -406,7 +421,15 @@ __global__ void sp_finish(const double* pb, int GB, const double* pc, int GC, in
   __shared__ double part[SP_KMAX];
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     double rs = 0.0;
-    for (int g = 0; g < GB; ++g) rs += pb[size_t(g) * K + k];
+    int g = 0;
+    for (; g + 7 < GB; g += 8) {   // 8 loads in flight, added in order
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = pb[size_t(g + u) * K + k];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) rs += v[u];
+    }
+    for (; g < GB; ++g) rs += pb[size_t(g) * K + k];
     denw[k] = rs;
     part[k] = (comm_a[k] / norms[k]) * rs;
   }
@@ -415,7 +438,15 @@ __global__ void sp_finish(const double* pb, int GB, const double* pc, int GC, in
     double dense = 0.0;
     for (int k = 0; k < K; ++k) dense += part[k];
     double s = 0.0;
-    for (int g = 0; g < GC; ++g) s += pc[g];
+    int g = 0;
+    for (; g + 7 < GC; g += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = pc[g + u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; g < GC; ++g) s += pc[g];
     comm_obj[0] = s;
     comm_obj[1] = dense;
   }

@@ -47,6 +47,7 @@ struct RunState {
   double elapsed;        // accumulated seconds (solver.py:302-312 timer)
   int converged;
   int pad;
+  unsigned long long t_last;   // sparse path: globaltimer at the last finished iteration
 };
 
 __device__ __forceinline__ bool iter_active(const RunState* st, int slot) {

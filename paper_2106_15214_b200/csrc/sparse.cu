@@ -20,8 +20,14 @@
 //   (+ allreduce N x K of the numerators when rows are sharded)
 //   pass B3 (column x k)             H_p = H~ * num/DenH, H~_p = H_p * norms,
 //                                    per-block rowsum of H~_p (next DenW)
-//   pass C  (CSR, warp per row)      W~_p = W_p / norms, objective at nonzeros
-//   finish                           objective + dense term, stop rule
+//   pass C  (CSR, warp per row)      W~_p = W_p / norms
+//   finish                           rowsum(H~_p), dense objective term
+// The nonzero part of the objective of iterate p needs W~_p H~_p at every
+// nonzero, which is the product pass A of iteration p+1 forms anyway: pass A
+// accumulates it there (bit for bit the sum a separate pass would give), and
+// the trace row / stop rule of iterate p run right after it.  A stop at p
+// skips the rest of slot p+1, so W~_p and H~_p stay the live iterate; one
+// trailing objective-only slot finishes the last iteration.
 //
 // Warp layout of the nonzero passes: 4 groups of 8 lanes, one nonzero per
 // group, each lane holding KPL consecutive k of the (KL = K rounded up to 32)
@@ -109,10 +115,20 @@ __device__ __forceinline__ float group_sum(float v) {
   return v;
 }
 
+// iterate base+slot-1 is finished in slot `slot` (lagged objective)
+__device__ __forceinline__ bool prev_live(const RunState* st, int slot) {
+  const long long it = st->base + slot - 1;
+  return it >= 1 && it <= st->stop_iter && it <= st->max_iter;
+}
+
 // ---- pass A: rows --------------------------------------------------------
 template <int KPL>
 __global__ void __launch_bounds__(SP_THREADS, 3) sp_pass_a(SpArgs a, const RunState* st, int slot) {
-  if (!iter_active(st, slot)) return;
+  const bool upd = iter_active(st, slot);   // W update of this iteration
+  const bool objp = prev_live(st, slot);    // objective of the previous iterate
+  if (!upd && !objp) return;
+  double acc = 0.0;
+  __shared__ double red[SP_THREADS / 8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane >> 3, sl = lane & 7, k0 = sl * KPL;
   const int KL = a.KL;
@@ -128,6 +144,7 @@ __global__ void __launch_bounds__(SP_THREADS, 3) sp_pass_a(SpArgs a, const RunSt
     ld_row<KPL>(a.Wt + size_t(f) * KL + k0, w);
 #pragma unroll
     for (int i = 0; i < KPL; ++i) num[i] = 0.f;
+    float rowacc = 0.f;
     const long long j0 = a.indptr[f], j1 = a.indptr[f + 1];
     for (long long jj = j0; jj < j1; jj += 4 * SP_U) {
       // SP_U nonzeros per group in flight: indices first, then the row gathers
@@ -149,18 +166,21 @@ __global__ void __launch_bounds__(SP_THREADS, 3) sp_pass_a(SpArgs a, const RunSt
 #pragma unroll
         for (int i = 0; i < KPL; ++i) p = fmaf(w[i], h[u][i], p);
         const float y = group_sum(p);
+        // x log(x / y) - x at the nonzero (core.py:101), iterate p-1
+        if (objp && x[u] != 0.f) rowacc += x[u] * logf(x[u] / y) - x[u];
         const float zz = ok ? x[u] / y : 0.f;
-        if (ok && sl == 0) a.z[j] = zz;
+        if (upd && ok && sl == 0) a.z[j] = zz;
 #pragma unroll
         for (int i = 0; i < KPL; ++i) num[i] = fmaf(zz, h[u][i], num[i]);
       }
     }
+    acc += double(rowacc);   // identical on the 8 lanes of a group
 #pragma unroll
     for (int i = 0; i < KPL; ++i) {   // groups 0..3 in a fixed tree
       num[i] += __shfl_xor_sync(0xffffffffu, num[i], 8);
       num[i] += __shfl_xor_sync(0xffffffffu, num[i], 16);
     }
-    if (grp == 0) {
+    if (upd && grp == 0) {
       float wn[KPL];
 #pragma unroll
       for (int i = 0; i < KPL; ++i) {
@@ -172,6 +192,15 @@ __global__ void __launch_bounds__(SP_THREADS, 3) sp_pass_a(SpArgs a, const RunSt
         }
       }
       st_row<KPL>(a.Wp + size_t(f) * KL + k0, wn);
+    }
+  }
+  if (objp) {   // per-block partial in a fixed order
+    if (sl == 0) red[threadIdx.x >> 3] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int i = 0; i < SP_THREADS / 8; ++i) t += red[i];
+      a.pc[blockIdx.x] = t;
     }
   }
 }
@@ -334,54 +363,14 @@ __global__ void __launch_bounds__(SP_THREADS) sp_pass_b3(SpArgs a, const RunStat
   }
 }
 
-// ---- pass C: normalise W, objective at the nonzeros ------------------------
-template <int KPL>
+// ---- pass C: normalise W ------------------------------------------------
 __global__ void __launch_bounds__(SP_THREADS) sp_pass_c(SpArgs a, const RunState* st, int slot) {
   if (!iter_active(st, slot)) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int grp = lane >> 3, sl = lane & 7, k0 = sl * KPL;
-  const int KL = a.KL;
-  double acc = 0.0;
-  __shared__ double red[SP_THREADS / 8];
-  double ninv[KPL];
-#pragma unroll
-  for (int i = 0; i < KPL; ++i) ninv[i] = k0 + i < a.K ? 1.0 / a.norms[k0 + i] : 0.0;
-  for (int f = blockIdx.x * SP_WARPS + warp; f < a.F; f += gridDim.x * SP_WARPS) {
-    float w[KPL];
-    ld_row<KPL>(a.Wp + size_t(f) * KL + k0, w);
-#pragma unroll
-    for (int i = 0; i < KPL; ++i) w[i] = float(double(w[i]) * ninv[i]);
-    if (grp == 0) st_row<KPL>(a.Wt + size_t(f) * KL + k0, w);
-    const long long j0 = a.indptr[f], j1 = a.indptr[f + 1];
-    float rowacc = 0.f;
-    for (long long jj = j0; jj < j1; jj += 4 * SP_U) {
-      int n[SP_U];
-      float x[SP_U], h[SP_U][KPL];
-#pragma unroll
-      for (int u = 0; u < SP_U; ++u) {
-        const long long j = jj + 4 * u + grp;
-        n[u] = j < j1 ? a.indices[j] : 0;
-        x[u] = j < j1 ? a.vals[j] : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < SP_U; ++u) ld_row<KPL>(a.Hn + size_t(n[u]) * KL + k0, h[u]);
-#pragma unroll
-      for (int u = 0; u < SP_U; ++u) {
-        float p = 0.f;
-#pragma unroll
-        for (int i = 0; i < KPL; ++i) p = fmaf(w[i], h[u][i], p);
-        const float y = group_sum(p);
-        if (x[u] != 0.f) rowacc += x[u] * logf(x[u] / y) - x[u];
-      }
-    }
-    acc += double(rowacc);   // identical on the 8 lanes of a group
-  }
-  if (sl == 0) red[threadIdx.x >> 3] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < SP_THREADS / 8; ++i) s += red[i];
-    a.pc[blockIdx.x] = s;
+  const size_t total = size_t(a.F) * a.KL;
+  for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < total;
+       t += size_t(gridDim.x) * blockDim.x) {
+    const int k = int(t % a.KL);
+    a.Wt[t] = k < a.K ? float(double(a.Wp[t]) * (1.0 / a.norms[k])) : 0.f;
   }
 }
 
@@ -412,11 +401,11 @@ __global__ void sp_post_a(const double* comm, int K, double* denh, double* norms
     norms[k] = sqrt(comm[K + k]);
   }
 }
-// rowsum(H~_p) -> denw (next iteration); local nonzero part of the objective
-// -> comm_obj[0], global dense part sum_k colsum(W~_p) rowsum(H~_p) -> comm_obj[1]
-__global__ void sp_finish(const double* pb, int GB, const double* pc, int GC, int K,
-                          const double* comm_a, const double* norms, double* denw,
-                          double* comm_obj, const RunState* st, int slot) {
+// rowsum(H~_p) -> denw (next iteration); global dense part of the objective of
+// iterate p, sum_k colsum(W~_p) rowsum(H~_p) -> comm_obj[1]
+__global__ void sp_finish(const double* pb, int GB, int K, const double* comm_a,
+                          const double* norms, double* denw, double* comm_obj, const RunState* st,
+                          int slot) {
   if (!iter_active(st, slot)) return;
   __shared__ double part[SP_KMAX];
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
@@ -437,23 +426,59 @@ __global__ void sp_finish(const double* pb, int GB, const double* pc, int GC, in
   if (threadIdx.x == 0) {
     double dense = 0.0;
     for (int k = 0; k < K; ++k) dense += part[k];
-    double s = 0.0;
-    int g = 0;
-    for (; g + 7 < GC; g += 8) {
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = pc[g + u];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) s += v[u];
-    }
-    for (; g < GC; ++g) s += pc[g];
-    comm_obj[0] = s;
     comm_obj[1] = dense;
   }
 }
+// local nonzero part of the objective of iterate base+slot-1 (pass A partials)
+// -> comm_obj[0]
+__global__ void sp_obj_prev(const double* pc, int GC, double* comm_obj, const RunState* st,
+                            int slot) {
+  if (!prev_live(st, slot)) return;
+  double s = 0.0;
+  int g = 0;
+  for (; g + 7 < GC; g += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = pc[g + u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; g < GC; ++g) s += pc[g];
+  comm_obj[0] = s;
+}
 __global__ void sp_total_obj(double* comm_obj, const RunState* st, int slot) {
-  if (!iter_active(st, slot)) return;
+  if (!prev_live(st, slot)) return;
   comm_obj[2] = comm_obj[0] + comm_obj[1];
+}
+__global__ void sp_begin(RunState* st, int slot) {
+  if (st->base + slot == 1) st->t_last = globaltimer();
+}
+// trace row + stop rule of iterate base+slot-1 (finish_iter, solver.py:309-319,
+// 174-180); the timer accumulates from the previous finish
+__global__ void sp_finish_prev(RunState* st, int slot, const double* __restrict__ obj,
+                               double* __restrict__ trace_obj, double* __restrict__ trace_sec,
+                               double tol) {
+  if (!prev_live(st, slot)) return;
+  const long long it = st->base + slot - 1;
+  const double o = *obj;
+  bool stop = false;
+  if (it > 1) {
+    const double prev = st->prev_obj;
+    if (o == prev) stop = true;
+    else if (o <= 0.0) stop = false;
+    else stop = (prev - o) / o <= tol;
+  }
+  const unsigned long long t = globaltimer();
+  st->elapsed += double(t - st->t_last) * 1e-9;
+  st->t_last = t;
+  trace_obj[it - 1] = o;
+  trace_sec[it - 1] = st->elapsed;
+  st->prev_obj = o;
+  st->iters_done = it;
+#ifdef BNMF_X_NOSTOP
+  stop = false;
+#endif
+  if (stop) { st->stop_iter = it; st->converged = 1; }
 }
 // rowsum(H~) of the initial iterate: per-block partials, then a fixed-order sum
 __global__ void sp_rowsum_part(const float* Ht, int N, int KL, int K, double* pb) {
@@ -801,10 +826,7 @@ struct SparseEngine : EngineBase {
       ++launches;
     }
   }
-  template <int KPL>
-  void launch_rows_c(const SpArgs& a, int slot) {
-    sp_pass_c<KPL><<<GA, SP_THREADS, 0, stream>>>(a, st, slot);
-  }
+
   void dispatch(int which, const SpArgs& a, int slot) {
     const int kpl = KL / 8;
     if (which == 0) {
@@ -816,16 +838,21 @@ struct SparseEngine : EngineBase {
       else if (kpl == 8) launch_b1<8>(a, slot);
       else launch_b1<16>(a, slot);
     } else {
-      if (kpl == 4) launch_rows_c<4>(a, slot);
-      else if (kpl == 8) launch_rows_c<8>(a, slot);
-      else launch_rows_c<16>(a, slot);
+      sp_pass_c<<<nsm * 8, SP_THREADS, 0, stream>>>(a, st, slot);
     }
   }
 
   int enqueue_iteration(int slot) {
     SpArgs a = args();
-    begin_iter<<<1, 1, 0, stream>>>(st, slot);
-    dispatch(0, a, slot);
+    double* cobj = comm + 2 * K;
+    sp_begin<<<1, 1, 0, stream>>>(st, slot);
+    dispatch(0, a, slot);   // W update of this iteration + objective of the previous iterate
+    sp_obj_prev<<<1, 1, 0, stream>>>(pc, GA, cobj, st, slot);
+    SCK(cudaGetLastError());
+    launches += 3;
+    if (int rc = allreduce(cobj, 1, ncclDouble)) return rc;   // nonzero part only
+    sp_total_obj<<<1, 1, 0, stream>>>(cobj, st, slot);
+    sp_finish_prev<<<1, 1, 0, stream>>>(st, slot, cobj + 2, tr_obj, tr_sec, sc.tol);
     sp_colstats<<<GS, SP_THREADS, 0, stream>>>(a, st, slot);
     sp_reduce_a<<<2 * K, 256, 0, stream>>>(pa, GS, K, comm, st, slot);
     SCK(cudaGetLastError());
@@ -840,13 +867,9 @@ struct SparseEngine : EngineBase {
     if (int rc = allreduce(num, size_t(N) * KL, ncclFloat)) return rc;
     sp_pass_b3<<<GB3, SP_THREADS, 0, stream>>>(a, st, slot);
     dispatch(2, a, slot);
-    double* cobj = comm + 2 * K;
-    sp_finish<<<1, 128, 0, stream>>>(pb, GB3, pc, GA, K, comm, norms, denw, cobj, st, slot);
+    sp_finish<<<1, 128, 0, stream>>>(pb, GB3, K, comm, norms, denw, cobj, st, slot);
     SCK(cudaGetLastError());
     launches += 3;
-    if (int rc = allreduce(cobj, 1, ncclDouble)) return rc;   // nonzero part only
-    sp_total_obj<<<1, 1, 0, stream>>>(cobj, st, slot);
-    finish_iter<<<1, 1, 0, stream>>>(st, slot, cobj + 2, tr_obj, tr_sec, sc.tol);
     // H~_p becomes the next iterate
     std::swap(Ht, Hn);
     SCK(cudaGetLastError());

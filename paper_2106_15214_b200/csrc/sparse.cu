@@ -127,8 +127,10 @@ __global__ void __launch_bounds__(SP_THREADS, 3) sp_pass_a(SpArgs a, const RunSt
   const bool upd = iter_active(st, slot);   // W update of this iteration
   const bool objp = prev_live(st, slot);    // objective of the previous iterate
   if (!upd && !objp) return;
-  double acc = 0.0;
+  // per-group running objective sums live in shared memory (registers are
+  // what bounds the rows in flight)
   __shared__ double red[SP_THREADS / 8];
+  if ((threadIdx.x & 7) == 0) red[threadIdx.x >> 3] = 0.0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane >> 3, sl = lane & 7, k0 = sl * KPL;
   const int KL = a.KL;
@@ -166,15 +168,15 @@ __global__ void __launch_bounds__(SP_THREADS, 3) sp_pass_a(SpArgs a, const RunSt
 #pragma unroll
         for (int i = 0; i < KPL; ++i) p = fmaf(w[i], h[u][i], p);
         const float y = group_sum(p);
-        // x log(x / y) - x at the nonzero (core.py:101), iterate p-1
-        if (objp && x[u] != 0.f) rowacc += x[u] * logf(x[u] / y) - x[u];
         const float zz = ok ? x[u] / y : 0.f;
+        // x log(x / y) - x at the nonzero (core.py:101), iterate p-1
+        if (objp && x[u] != 0.f) rowacc += x[u] * logf(zz) - x[u];
         if (upd && ok && sl == 0) a.z[j] = zz;
 #pragma unroll
         for (int i = 0; i < KPL; ++i) num[i] = fmaf(zz, h[u][i], num[i]);
       }
     }
-    acc += double(rowacc);   // identical on the 8 lanes of a group
+    if (objp && sl == 0) red[threadIdx.x >> 3] += double(rowacc);
 #pragma unroll
     for (int i = 0; i < KPL; ++i) {   // groups 0..3 in a fixed tree
       num[i] += __shfl_xor_sync(0xffffffffu, num[i], 8);
@@ -195,7 +197,6 @@ __global__ void __launch_bounds__(SP_THREADS, 3) sp_pass_a(SpArgs a, const RunSt
     }
   }
   if (objp) {   // per-block partial in a fixed order
-    if (sl == 0) red[threadIdx.x >> 3] = acc;
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0;

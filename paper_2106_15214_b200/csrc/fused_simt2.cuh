@@ -113,7 +113,7 @@ __device__ __forceinline__ float zdiv(float x, float y, float beta, float& zn, f
 }
 
 // y[i][j] = sum_k Ws[r_i][k] * Hs[c_j][k], rows r_i = 4 tf + i, columns
-// c_0 = tn, c_1 = tn + 16; k in ascending order (same order as the SIMT twin)
+// c_0 = tn, c_1 = tn + 16; k in ascending order
 __device__ __forceinline__ void vt_tile(const float* Ws, const float* Hs, int rs, int kr, int tf,
                                         int tn, float (&y)[4][2]) {
 #pragma unroll

@@ -1,5 +1,5 @@
 // tcgen05 implementation of the fused single-read pass (fp32, rank K <= 16,
-// F <= 256).  Same contract as fused_pass_simt (fused_common.cuh).
+// F <= 256).  Same contract as the SIMT pair fs2::hpass + fs2::wpass (fused_common.cuh).
 //
 // Rows of V are split over a cluster of CL CTAs (CL = 2 when F > 128): CTA r
 // owns rows [row0, row0 + FTr) and every column block of its cluster, so

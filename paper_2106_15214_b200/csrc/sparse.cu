@@ -365,13 +365,27 @@ __global__ void __launch_bounds__(SP_THREADS) sp_pass_b3(SpArgs a, const RunStat
 }
 
 // ---- pass C: normalise W ------------------------------------------------
+// W~_p = W_p / norms, float4 per thread, rows grid-strided (no index divides)
 __global__ void __launch_bounds__(SP_THREADS) sp_pass_c(SpArgs a, const RunState* st, int slot) {
   if (!iter_active(st, slot)) return;
-  const size_t total = size_t(a.F) * a.KL;
-  for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < total;
-       t += size_t(gridDim.x) * blockDim.x) {
-    const int k = int(t % a.KL);
-    a.Wt[t] = k < a.K ? float(double(a.Wp[t]) * (1.0 / a.norms[k])) : 0.f;
+  const int KL4 = a.KL >> 2, rpb = SP_THREADS / KL4;
+  const int k4 = threadIdx.x % KL4, r = threadIdx.x / KL4;
+  if (r >= rpb) return;
+  double ninv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int k = 4 * k4 + i;
+    ninv[i] = k < a.K ? 1.0 / a.norms[k] : 0.0;
+  }
+  const bool pad[4] = {4 * k4 >= a.K, 4 * k4 + 1 >= a.K, 4 * k4 + 2 >= a.K, 4 * k4 + 3 >= a.K};
+  for (size_t f = blockIdx.x * size_t(rpb) + r; f < size_t(a.F); f += size_t(gridDim.x) * rpb) {
+    const float4 w = *reinterpret_cast<const float4*>(a.Wp + f * a.KL + 4 * k4);
+    float4 o;
+    o.x = pad[0] ? 0.f : float(double(w.x) * ninv[0]);
+    o.y = pad[1] ? 0.f : float(double(w.y) * ninv[1]);
+    o.z = pad[2] ? 0.f : float(double(w.z) * ninv[2]);
+    o.w = pad[3] ? 0.f : float(double(w.w) * ninv[3]);
+    *reinterpret_cast<float4*>(a.Wt + f * a.KL + 4 * k4) = o;
   }
 }
 

@@ -57,6 +57,8 @@ constexpr int SP_SEG = 2048;   // nonzeros per column segment (pass B1)
 // W~ rows they gather stay in L2 (one 16 MB tile of W~ at K = 64) instead of
 // being fetched from HBM once per nonzero.
 constexpr int SP_HEAVY = 2048;
+// columns with more segments than this are summed by pass B2h (a block each)
+constexpr int SP_B2_HEAVY = 64;
 constexpr int SP_TILE = 131072;
 constexpr int SP_SEG_H = 512;  // heavy-column segments (more warps per tile)
 #ifndef BNMF_SP_U
@@ -76,6 +78,8 @@ struct SpArgs {
   const int* colseg;           // [N + 1] each column's run in seglist
   const int* seglist;          // [S] segment ids of each column, in row order
   int S;
+  const int* hcols;            // columns with > SP_B2_HEAVY segments (pass B2h)
+  int NH;
   float* z;                    // per nonzero (CSR order)
   float* Wt;                   // W~ (F x KL)
   float* Wp;                   // W_p (F x KL)
@@ -311,6 +315,7 @@ __global__ void sp_pass_b2(SpArgs a, const RunState* st, int slot) {
        t += size_t(gridDim.x) * blockDim.x) {
     const int n = int(t / a.KL), k = int(t - size_t(n) * a.KL);
     const int s0 = a.colseg[n], s1 = a.colseg[n + 1];
+    if (s1 - s0 > SP_B2_HEAVY) continue;   // pass B2h
     float v = a.part[size_t(a.seglist[s0]) * a.KL + k];
     if (s1 - s0 > 1) {
       // same left-to-right order as a plain loop (bitwise identical), but the
@@ -333,6 +338,43 @@ __global__ void sp_pass_b2(SpArgs a, const RunState* st, int slot) {
       v = float(acc);
     }
     a.num[t] = v;
+  }
+}
+
+// ---- pass B2h: the Zipf-heavy columns, one block each ----------------------
+// thread (k, p): p-th contiguous run of the column's segments after the first,
+// summed in order; the runs are then added to the first segment in p order
+// (a fixed order, so deterministic)
+__global__ void __launch_bounds__(1024) sp_pass_b2h(SpArgs a, const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  __shared__ double red[1024];
+  const int KL = a.KL, P = blockDim.x / KL;
+  const int k = threadIdx.x % KL, p = threadIdx.x / KL;
+  const int n = a.hcols[blockIdx.x];
+  const int s0 = a.colseg[n], s1 = a.colseg[n + 1];
+  const int L = s1 - s0 - 1, per = (L + P - 1) / P;
+  double acc = 0.0;
+  if (p < P) {
+    int s = s0 + 1 + p * per;
+    const int e = min(s1, s + per);
+    for (; s + 8 <= e; s += 8) {
+      int id[8];
+      float pv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) id[i] = a.seglist[s + i];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) pv[i] = a.part[size_t(id[i]) * KL + k];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc += double(pv[i]);
+    }
+    for (; s < e; ++s) acc += double(a.part[size_t(a.seglist[s]) * KL + k]);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (p == 0) {
+    double t = double(a.part[size_t(a.seglist[s0]) * KL + k]);
+    for (int q = 0; q < P; ++q) t += red[q * KL + k];
+    a.num[size_t(n) * KL + k] = float(t);
   }
 }
 
@@ -577,6 +619,8 @@ struct SparseEngine : EngineBase {
   int* segcol = nullptr;
   int* colseg = nullptr;
   int* seglist = nullptr;
+  int* hcols = nullptr;
+  int NH = 0;
   std::vector<int> tstart;   // [ntile + 2] B1 launch ranges of segments
   float *z = nullptr, *Wt = nullptr, *Wp = nullptr, *Ht = nullptr, *Hn = nullptr;
   float *part = nullptr, *num = nullptr;
@@ -600,7 +644,7 @@ struct SparseEngine : EngineBase {
   }
   ~SparseEngine() override {
     if (gexec) cudaGraphExecDestroy(gexec);
-    void* ptrs[] = {indptr, indices, vals, rowidx, perm, segptr, segcol, colseg, seglist, z, Wt, Wp, Ht,
+    void* ptrs[] = {indptr, indices, vals, rowidx, perm, segptr, segcol, colseg, seglist, hcols, z, Wt, Wp, Ht,
                     Hn, part, num, denw, denh, norms, pa, pb, pc, comm, tr_obj, tr_sec, tr_kkt, st};
     for (void* q : ptrs) if (q) cudaFree(q);
     if (st_host) cudaFreeHost(st_host);
@@ -705,6 +749,13 @@ struct SparseEngine : EngineBase {
     if ((rc = upload(&segcol, scol.data(), scol.size(), 0))) return rc;
     if ((rc = upload(&colseg, cs.data(), cs.size(), 0))) return rc;
     if ((rc = upload(&seglist, sl.data(), sl.size(), 0))) return rc;
+    {
+      std::vector<int> hc;
+      for (int n = 0; n < N; ++n)
+        if (cs[n + 1] - cs[n] > SP_B2_HEAVY) hc.push_back(n);
+      NH = int(hc.size());
+      if ((rc = upload(&hcols, hc.data(), hc.size(), 0))) return rc;
+    }
     if (z) SCK(cudaFree(z));
     z = nullptr;
     SCK(cudaMalloc(&z, std::max<size_t>(nnz, 1) * sizeof(float)));
@@ -773,6 +824,7 @@ struct SparseEngine : EngineBase {
     a.indptr = indptr; a.indices = indices; a.vals = vals;
     a.rowidx = rowidx; a.perm = perm;
     a.segptr = segptr; a.segcol = segcol; a.colseg = colseg; a.seglist = seglist; a.S = S;
+    a.hcols = hcols; a.NH = NH;
     a.z = z;
     a.Wt = Wt; a.Wp = Wp; a.Ht = Ht; a.Hn = Hn; a.part = part; a.num = num;
     a.denw = denw; a.denh = denh; a.norms = norms;
@@ -876,6 +928,10 @@ struct SparseEngine : EngineBase {
     sp_post_a<<<1, 128, 0, stream>>>(comm, K, denh, norms, st, slot);
     dispatch(1, a, slot);
     sp_pass_b2<<<nsm * 8, 256, 0, stream>>>(a, st, slot);
+    if (NH > 0) {
+      sp_pass_b2h<<<NH, 1024, 0, stream>>>(a, st, slot);
+      ++launches;
+    }
     SCK(cudaGetLastError());
     launches += 3;
     // rows are sharded: every rank holds a partial H numerator of its rows

@@ -143,63 +143,110 @@ class ClockSampler:
                 "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
 
 
-def cpu_sample(cfg_id, algo, iters=3, n_sample=None):
-    """The oracle (numpy port of the reference loop) on a bounded column prefix,
-    all host cores for BLAS; returns (iterations/s scaled to full N, info)."""
-    from threadpoolctl import threadpool_limits
+def _import_reference():
+    """The unmodified reference package installed under baseline/_ref (pip
+    --target of /root/reference/pkg; git-ignored, travels to the GPU box), or
+    None when it is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "betanmf")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import betanmf
+        import betanmf.solver
+        return betanmf
+    except Exception:
+        return None
 
-    from oracle import betanmf_oracle as O
+
+def reference_sample_cols(cfg_id):
+    """Columns of the bounded CPU sample: a 65536-column prefix of config 4
+    (1/64 of the workload; columns are independent given W, so the time per
+    iteration is linear in N), the whole matrix otherwise."""
     c = CONFIGS[cfg_id]
+    return min(c["N"], 65536) if cfg_id == 4 else c["N"]
+
+
+def time_reference(cfg_id, algo, warmup, steps):
+    """Time the reference's own CPU loop on the bounded sample; returns
+    (seconds per outer iteration on the sample, info dict)."""
+    c = CONFIGS[cfg_id]
+    from threadpoolctl import threadpool_limits, threadpool_info
+
     cores = os.cpu_count() or 1
-    n_sample = n_sample or (min(c["N"], 65536) if cfg_id == 4 else c["N"])
-    v = make_data(cfg_id, 0, n_sample, "fp64" if c["dtype"] == "fp64" else "fp32")
-    v = v.astype(np.float64)
-    w0, h0 = make_init(cfg_id, 0, n_sample)
-    with threadpool_limits(limits=cores):
-        O.run(v, c["beta"], c["K"], algo, kappa=c["kappa"], tol=1e-300, max_outer_iters=1,
-              init=(w0, h0), kkt=False)  # warm
-        t0 = time.perf_counter()
-        O.run(v, c["beta"], c["K"], algo, kappa=c["kappa"], tol=1e-300, max_outer_iters=iters,
-              init=(w0, h0), kkt=False)
-        dt = (time.perf_counter() - t0) / iters
+    n_sample = reference_sample_cols(cfg_id)
     scale = c["N"] / n_sample
-    return 1.0 / (dt * scale), dict(cores=cores, n_sample=n_sample, s_per_iter_sample=dt,
-                                   scale=scale)
+    v = make_data(cfg_id, 0, n_sample, c["dtype"]).astype(np.float64)
+    w0, h0 = make_init(cfg_id, 0, n_sample)
+    iters = warmup + steps
+    ref = _import_reference()
+    t_wall = time.perf_counter()
+    with threadpool_limits(limits=cores):
+        blas_threads = max([d.get("num_threads", 0) for d in threadpool_info()] or [0])
+        if ref is not None:
+            kind = "reference"
+            saved = ref.solver.init_factors
+            ref.solver.init_factors = lambda F, N, K, seed: ref.FactorPair(w0.copy(), h0.copy())
+            try:
+                cfg = ref.SolverConfig(beta=c["beta"], rank=c["K"], algorithm=algo,
+                                       kappa=c["kappa"], tol=1e-300, max_outer_iters=iters)
+                res = ref.fit(v, cfg)
+            finally:
+                ref.solver.init_factors = saved
+            secs = np.array([r.seconds for r in res.trace])
+            times = np.diff(np.concatenate([[0.0], secs]))[warmup:]
+            what = "betanmf.fit (unmodified reference, baseline/_ref), TraceRow.seconds"
+        else:
+            kind = "port"
+            from oracle import betanmf_oracle as O
+            times = []
+            w, h = w0, h0
+            for i in range(iters):
+                t0 = time.perf_counter()
+                w, h, _, _, _ = O.run(v, c["beta"], c["K"], algo, kappa=c["kappa"],
+                                      tol=1e-300, max_outer_iters=1, init=(w, h), kkt=False)
+                if i >= warmup:
+                    times.append(time.perf_counter() - t0)
+            times = np.array(times)
+            what = "numpy port of the reference loop (oracle/betanmf_oracle.py), perf_counter"
+    wall = time.perf_counter() - t_wall
+    dt = float(np.mean(times))
+    sample = (f"{what}; fp64; {c['F']}x{n_sample} column prefix of {c['F']}x{c['N']} "
+              f"(1/{scale:g} of the workload); each step = one outer iteration on the prefix, "
+              f"measured {dt * 1e3:.1f} ms; value = 1 / (that x {scale:g})")
+    return dt, dict(cores=cores, kind=kind, n_sample=n_sample, scale=scale, sample=sample,
+                    wall_s=round(wall, 2), blas_threads=blas_threads)
 
 
 def run_reference(args):
+    """Reference arm: the reference's own CPU loop on the box's host cores.
+
+    With baseline/_ref present this is the unmodified ``betanmf.fit``
+    (run_jmm / run_bmm) with the bench's injected Uniform(0,1) init
+    (monkeypatched ``init_factors``, as tests/golden/gen_golden.py does), timed
+    by the reference's own loop timer (``TraceRow.seconds``: monotonic, KKT
+    excluded, solver.py:302-312), BLAS on every host core; otherwise the
+    numpy port in oracle/.  Each step is one outer iteration on the bounded
+    sample (reference_sample_cols); ``ms_per_step`` is that measured time and
+    ``value`` the iterations/s it implies for the full workload."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    c = CONFIGS[args.config]
-    from threadpoolctl import threadpool_limits
-
-    from oracle import betanmf_oracle as O
-    cores = os.cpu_count() or 1
-    n_sample = min(c["N"], 65536) if args.config == 4 else c["N"]
-    v = make_data(args.config, 0, n_sample, c["dtype"]).astype(np.float64)
-    w0, h0 = make_init(args.config, 0, n_sample)
-    times = []
-    with threadpool_limits(limits=cores):
-        w, h = w0, h0
-        for i in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            w, h, _, _, _ = O.run(v, c["beta"], c["K"], args.algo, kappa=c["kappa"], tol=1e-300,
-                                  max_outer_iters=1, init=(w, h), kkt=False)
-            if i >= args.warmup:
-                times.append(time.perf_counter() - t0)
-    dt = sum(times) / len(times) * (c["N"] / n_sample)
-    val = 1.0 / dt
-    sample = (f"numpy oracle port of the reference loop, fp64, {c['F']}x{n_sample} column prefix "
-              f"(of N={c['N']}), per-iteration time scaled x{c['N'] / n_sample:g}")
+    dt, info = time_reference(args.config, args.algo, args.warmup, args.steps)
+    val = 1.0 / (dt * info["scale"])
     out = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "iterations/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, world),
-        "cpu_baseline": {"value": val, "unit": "iterations/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+        "sample": {"n_cols": info["n_sample"], "scale_to_workload": info["scale"],
+                   "ms_per_step_on_sample": dt * 1e3,
+                   "ms_per_full_iteration": dt * info["scale"] * 1e3,
+                   "wall_s": info["wall_s"], "blas_threads": info["blas_threads"]},
+        "cpu_baseline": {"value": val, "unit": "iterations/s", "cores": info["cores"],
+                         "kind": info["kind"], "sample": info["sample"]},
         "e2e": {"value": val, "unit": "iterations/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -259,6 +306,9 @@ def main():
     pass_ms, pass_samples = ctx.pass_time()
     ctx.set_profiling(False)   # the e2e leg below runs without per-pass events
     done, _ = ctx.sync()
+    if done != args.warmup + args.steps:
+        raise RuntimeError(f"only {done} of {args.warmup + args.steps} iterations ran (the stop "
+                           "rule fired); the timed region would include no-op slots")
     obj, _, _ = ctx.trace(done)
     launches = ctx.launches_per_iter()
     sched = ctx.schedule()
@@ -337,15 +387,15 @@ def main():
         "config": workload_config(args, world), "schedule": sched,
         "gpu_launches": launches * args.steps, "roofline": roofline,
         "clocks": clocks.summary(), "final_objective": float(obj[-1]) if done else None,
+        "iterations_done": int(done),
     }
     if e2e:
         out["e2e"] = e2e
     if world == 1 and not args.no_cpu:
-        val, info = cpu_sample(args.config, args.algo)
+        dt, info = time_reference(args.config, args.algo, 1, 3)
         out["cpu_baseline"] = {
-            "value": val, "unit": "iterations/s", "cores": info["cores"], "kind": "port",
-            "sample": f"numpy oracle (reference loop restated), fp64, {c['F']}x{info['n_sample']} "
-                      f"prefix, 3 iterations, scaled x{info['scale']:g} to N={c['N']}"}
+            "value": 1.0 / (dt * info["scale"]), "unit": "iterations/s", "cores": info["cores"],
+            "kind": info["kind"], "sample": info["sample"]}
     print(json.dumps(out))
 
 

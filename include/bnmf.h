@@ -135,6 +135,11 @@ int bnmf_active_schedule(bnmf_ctx* ctx, int* schedule);
  * bnmf_pass_time returns its average device time over the last chunk. */
 int bnmf_set_profiling(bnmf_ctx* ctx, int on);
 int bnmf_pass_time(bnmf_ctx* ctx, float* ms_avg, int* samples);
+/* Which fused pass kernel the last begin() selected: out[0] = 0 (none: reference
+ * schedule), 1 (SIMT pair) or 2 (tcgen05); out[1] = grid CTAs; out[2] = CTAs per
+ * cluster; out[3] = rows owned by cluster rank 0.  Diagnostics for the parity
+ * tests (BNMF_TC_MAX_CLUSTERS caps the tcgen05 grid). */
+int bnmf_pass_info(bnmf_ctx* ctx, int* out4);
 void* bnmf_stream(bnmf_ctx* ctx);
 
 #ifdef __cplusplus

@@ -78,6 +78,7 @@ _SIGS = {
     "bnmf_stream": ([C.c_void_p], C.c_void_p),
     "bnmf_set_profiling": ([C.c_void_p, C.c_int], C.c_int),
     "bnmf_pass_time": ([C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_int)], C.c_int),
+    "bnmf_pass_info": ([C.c_void_p, C.POINTER(C.c_int)], C.c_int),
     "bnmf_data_stats": ([C.c_void_p, C.POINTER(C.c_double)], C.c_int),
 }
 
@@ -269,6 +270,13 @@ class Context:
         n = C.c_int(0)
         self._check(self.lib.bnmf_pass_time(self.h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
+
+    def pass_info(self):
+        """(kernel, grid CTAs, CTAs per cluster, rows of cluster rank 0) of the fused pass
+        the last begin() selected; kernel is "none", "simt" or "tcgen05"."""
+        out = (C.c_int * 4)()
+        self._check(self.lib.bnmf_pass_info(self.h, out))
+        return {0: "none", 1: "simt", 2: "tcgen05"}[out[0]], out[1], out[2], out[3]
 
     def schedule(self):
         n = C.c_int(0)

@@ -775,6 +775,11 @@ struct Engine : EngineBase {
     return 0;
   }
 
+  void pass_info(int* out4) override {
+    if (fused_active && fused) fused_info(fused, out4);
+    else out4[0] = out4[1] = out4[2] = out4[3] = 0;
+  }
+
   int pass_time(float* ms_avg, int* samples) override {
     CK(cudaStreamSynchronize(stream));
     double tot = 0.0;
@@ -892,9 +897,19 @@ int bnmf_set_csr(bnmf_ctx* ctx, const int64_t* indptr, const int32_t* indices,
     cudaStream_t s;
     if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess)
       return set_err("stream create", BNMF_E_CUDA);
-    ctx->eng.reset(make_sparse_engine(dev, s));
+    std::unique_ptr<EngineBase> sp(make_sparse_engine(dev, s));
+    // a communicator attached before the switch moves to the sparse engine
+    // (the dense engine's destructor would otherwise destroy it)
+    sp->rank = ctx->eng->rank;
+    sp->nranks = ctx->eng->nranks;
+    sp->n_global = ctx->eng->n_global;
+    sp->comm_nccl = ctx->eng->comm_nccl;
+    ctx->eng->comm_nccl = nullptr;
+    ctx->eng = std::move(sp);
     ctx->sparse = true;
   }
+  if (nnz >= int64_t(INT32_MAX))
+    return set_err("the sparse path takes fewer than 2^31 - 1 nonzeros", BNMF_E_UNSUPPORTED);
   return sparse_set_csr(ctx->eng.get(), reinterpret_cast<const long long*>(indptr), indices,
                         values, reinterpret_cast<const long long*>(colptr), rowidx, perm, F, N,
                         nnz, src_on_device);
@@ -994,6 +1009,13 @@ int bnmf_pass_time(bnmf_ctx* ctx, float* ms_avg, int* samples) {
 int bnmf_active_schedule(bnmf_ctx* ctx, int* schedule) {
   CTX_CHECK(ctx);
   *schedule = ctx->eng->active_schedule;
+  return 0;
+}
+
+int bnmf_pass_info(bnmf_ctx* ctx, int* out4) {
+  CTX_CHECK(ctx);
+  if (!out4) return set_err("null output", BNMF_E_ARG);
+  ctx->eng->pass_info(out4);
   return 0;
 }
 

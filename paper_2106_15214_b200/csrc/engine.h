@@ -43,6 +43,9 @@ struct EngineBase {
   virtual int init_comm(int rank, int nranks, const void* id, int64_t n_global) = 0;
   virtual int set_profiling(int on) = 0;
   virtual int pass_time(float* ms_avg, int* samples) = 0;
+  // [kind (0 none, 1 SIMT pair, 2 tcgen05), grid CTAs, cluster size, rows of cluster rank 0]
+  // of the fused pass the last begin() selected
+  virtual void pass_info(int* out4) { out4[0] = out4[1] = out4[2] = out4[3] = 0; }
 };
 
 // What the fused fp32 pass needs from the engine (device pointers are owned by
@@ -91,5 +94,6 @@ int fused_export(FusedState* fs, const FusedIO& io, std::string& err);
 int fused_select(FusedState* fs, const FusedIO& io, std::string& err);  // async, no sync
 void fused_destroy(FusedState* fs);
 bool fused_shape_matches(const FusedState* fs, int F, int N, int K);
+void fused_info(const FusedState* fs, int* out4);
 
 }  // namespace bnmf

@@ -35,7 +35,6 @@ struct FusedArgs {
   int algorithm;          // 0 jmm, 1 bmm
   int do_h;               // 0 = prologue (W-side + objective only)
   int den_ones;           // beta == 1: H den = colsum(C2), W den = rowsum(H~)
-  int debug;              // tcgen05 pass bring-up knobs
   long long* prof;        // optional per-CTA wait-cycle counters [G][48] (BNMF_TC_PROF=1)
   Scalars sc;
 };

@@ -49,7 +49,13 @@ struct FusedState {
   size_t tc_smem = 0;
   CUtensorMap mapV;
   long long* prof = nullptr;   // BNMF_TC_PROF=1: wait-cycle counters [grid][48]
+  int cap = 0;                 // BNMF_TC_MAX_CLUSTERS at creation (test knob)
 };
+
+static int env_cluster_cap() {
+  const char* c = getenv("BNMF_TC_MAX_CLUSTERS");
+  return c ? std::max(0, atoi(c)) : 0;
+}
 
 static FusedState* g_last_tc = nullptr;
 
@@ -197,6 +203,10 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
         clusters = std::min(clusters, maxc);
       cudaGetLastError();
     }
+    // test knob: cap the grid so that every cluster walks many column blocks
+    // (the steady-state schedule of a full-size pass on a small matrix)
+    fs->cap = env_cluster_cap();
+    if (fs->cap > 0) clusters = std::min(clusters, fs->cap);
     fs->tc_grid = fs->tc_cl * std::max(1, std::min(nb, clusters));
   }
   int gmax = std::max(fs->tc_grid, fs->s2_S);
@@ -253,8 +263,6 @@ static FusedArgs make_args(FusedState* fs, const FusedIO& io, int do_h) {
   a.do_h = do_h;
   a.den_ones = beta_class(io.sc.beta) == BC_1 ? 1 : 0;
   a.sc = io.sc;
-  const char* dbg = getenv("BNMF_TC_DEBUG");
-  a.debug = dbg ? atoi(dbg) : 0;
   a.prof = fs->prof;
   return a;
 }
@@ -360,7 +368,14 @@ static int enqueue_pass_and_update(FusedState* fs, const FusedIO& io, int slot, 
 }
 
 bool fused_shape_matches(const FusedState* fs, int F, int N, int K) {
-  return fs && fs->F == F && fs->N == N && fs->K == K;
+  return fs && fs->F == F && fs->N == N && fs->K == K && (!fs->tc || fs->cap == env_cluster_cap());
+}
+
+void fused_info(const FusedState* fs, int* out4) {
+  out4[0] = fs ? (fs->tc ? 2 : 1) : 0;
+  out4[1] = fs ? (fs->tc ? fs->tc_grid : fs->s2_S * fs->s2_rc) : 0;
+  out4[2] = fs ? (fs->tc ? fs->tc_cl : 1) : 0;
+  out4[3] = fs ? (fs->tc ? fs->tc_f0 : fs->F) : 0;
 }
 
 int fused_begin(FusedState* fs, const FusedIO& io, std::string& err) {

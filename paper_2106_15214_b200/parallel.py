@@ -89,6 +89,27 @@ def resolve_kappa_global(values, beta, kappa):
     return 1e-9 * gsum / gcnt
 
 
+def agree_on_error(local_err):
+    """Collective error agreement: if any rank's input checks failed, every
+    rank raises (the failing rank its own error, the others a ValueError
+    naming the failing ranks), so no rank is left waiting in the next
+    collective."""
+    info = dist_info()
+    if info is None:
+        if local_err is not None:
+            raise local_err
+        return
+    rank, world = info
+    flags = np.zeros(world)
+    flags[rank] = 1.0 if local_err is not None else 0.0
+    flags = allreduce_scalars(flags, "sum")
+    if local_err is not None:
+        raise local_err
+    bad = [r for r in range(world) if flags[r] > 0]
+    if bad:
+        raise ValueError(f"input checks failed on rank(s) {bad}")
+
+
 def broadcast_uid(make_uid):
     """Rank 0 creates the NCCL unique id (128 bytes); everyone receives it."""
     import torch.distributed as dist

@@ -199,26 +199,10 @@ def _upload_checked(ctx, values, config):
     kappa = config.kappa
     ctx.set_dense(values, 0.0 if kappa is None else kappa)
     vmin, _vmax, vsum, nonfinite, count = ctx.data_stats()
-    if nonfinite > 0:
-        raise ValueError("data entries must be finite")
-    if vmin < 0.0:
-        raise ValueError("data entries must be nonnegative")
-    if kappa is None:
-        # default_kappa (core.py:176-185)
-        kappa = 0.0 if (1.0 <= config.beta <= 2.0 and vmin > 0.0) else 1e-9 * (vsum / count)
-        if kappa != 0.0:
-            ctx.set_dense(values, kappa)
-    kappa = float(kappa)
-    if not np.isfinite(kappa) or kappa < 0.0:
-        raise ValueError("kappa must be a nonnegative finite real")
-    if config.beta < 1.0 and kappa == 0.0 and vmin == 0.0:
-        raise DivergenceDomainError(
-            f"data contains zeros, which is outside the domain of "
-            f"d_beta for beta={config.beta}; set a positive kappa shift")
-    if config.beta <= 0.0 and vmin + kappa <= 0.0:
-        raise DivergenceDomainError(
-            f"data entries must be positive for beta={config.beta}; "
-            f"set a positive kappa shift")
+    kappa_in = kappa
+    kappa = _check_global(vmin, nonfinite, vsum, count, config, kappa)
+    if kappa_in is None and kappa != 0.0:
+        ctx.set_dense(values, kappa)
     F, N = values.shape
     return _Checked((F, N), kappa), F, N
 
@@ -339,30 +323,13 @@ def _run(data, config, counter, algorithm, *, dtype="fp64", init=None, device=No
                          f"run_{algorithm.value}")
     if dtype not in ("fp64", "fp32"):
         raise ValueError("dtype must be 'fp64' or 'fp32'")
-    n0 = 0
     if sharded:
         # `data` is this rank's column block; kappa and the init are global
-        from . import parallel
-        if parallel.dist_info() is None:
-            raise ValueError("sharded=True needs an initialised torch.distributed group")
-        vals = data.values if isinstance(data, DataMatrix) else np.asarray(data)
-        n0, n_global = parallel.column_offsets(vals.shape[1])
-        kappa = parallel.resolve_kappa_global(vals, config.beta, config.kappa if config.kappa
-                                              is not None else (data.kappa if isinstance(
-                                                  data, DataMatrix) else None))
-        import dataclasses
-        data = _prepare(DataMatrix(vals, kappa), dataclasses.replace(config, kappa=kappa))
-        F, N = data.shape
-        if init is None:
-            pair = init_factors(F, n_global, config.rank, config.seed)
-            init = (pair.w, pair.h)
-        w0, h0 = init if not isinstance(init, FactorPair) else (init.w, init.h)
-        w0, h0 = parallel.slice_init(w0, h0, n0, N, n_global)
-        pair = _resolve_init((w0, h0), F, N, config.rank, config.seed)
-    elif isinstance(data, DataMatrix) or np.asarray(data).size < _DEVICE_CHECK_MIN:
+        return _run_sharded_dense(data, config, counter, dtype=dtype, init=init, device=device,
+                                  kkt=kkt, schedule=schedule)
+    if isinstance(data, DataMatrix) or np.asarray(data).size < _DEVICE_CHECK_MIN:
         data = _prepare(data, config)
         F, N = data.shape
-        n_global = N
         pair = _resolve_init(init, F, N, config.rank, config.seed)
     else:
         # plain array: the DataMatrix checks run on device statistics of the
@@ -371,11 +338,8 @@ def _run(data, config, counter, algorithm, *, dtype="fp64", init=None, device=No
         data = None
     ctx = get_context(device, dtype)
     with ctx.lock:
-        if sharded:
-            _attach_comm(ctx, n_global)
         if data is None:
             data, F, N = _upload_checked(ctx, values, config)
-            n_global = N
             pair = _resolve_init(init, F, N, config.rank, config.seed, device_checked=True)
         else:
             ctx.set_dense(data.values, data.kappa)
@@ -391,6 +355,97 @@ def _run(data, config, counter, algorithm, *, dtype="fp64", init=None, device=No
     # fp32 entry underflows to 0, which is reported as is): no host re-scan
     factors = _unchecked_pair(w, h)
     return FitResult(factors=factors, trace=trace,
+                     termination=Termination.CONVERGED if converged else Termination.MAX_ITERS,
+                     iterations=done, config=config)
+
+
+def _check_global(vmin, nonfinite, vsum, count, config, kappa):
+    """The checks of DataMatrix / check_domain / _prepare (core.py:188-228,
+    solver.py:205-221) on statistics of the whole (possibly sharded) matrix;
+    returns the resolved kappa."""
+    if nonfinite > 0:
+        raise ValueError("data entries must be finite")
+    if vmin < 0.0:
+        raise ValueError("data entries must be nonnegative")
+    if kappa is None:
+        # default_kappa (core.py:176-185)
+        kappa = 0.0 if (1.0 <= config.beta <= 2.0 and vmin > 0.0) else 1e-9 * (vsum / count)
+    kappa = float(kappa)
+    if not np.isfinite(kappa) or kappa < 0.0:
+        raise ValueError("kappa must be a nonnegative finite real")
+    if config.beta < 1.0 and kappa == 0.0 and vmin == 0.0:
+        raise DivergenceDomainError(
+            f"data contains zeros, which is outside the domain of "
+            f"d_beta for beta={config.beta}; set a positive kappa shift")
+    if config.beta <= 0.0 and vmin + kappa <= 0.0:
+        raise DivergenceDomainError(
+            f"data entries must be positive for beta={config.beta}; "
+            f"set a positive kappa shift")
+    return kappa
+
+
+def _run_sharded_dense(data, config, counter, *, dtype, init, device, kkt, schedule):
+    """N-column sharded fit: this rank's column block of V.
+
+    Every rank uploads its block and reads device statistics of it
+    (bnmf_data_stats: min, non-finite count, fp64 sum); the statistics are
+    allreduced, so every rank applies the reference's checks to the same
+    global numbers and raises the same error before any communicator exists
+    (no rank can be left waiting in a collective)."""
+    from . import parallel
+    if parallel.dist_info() is None:
+        raise ValueError("sharded=True needs an initialised torch.distributed group")
+    if isinstance(data, DataMatrix):
+        vals = data.values
+        kappa = config.kappa if config.kappa is not None else data.kappa
+    else:
+        vals = np.asarray(data)
+        kappa = config.kappa
+    if vals.dtype not in (np.float64, np.float32):
+        vals = vals.astype(np.float64)
+    # shape errors are local: agree on them first
+    local_err = None
+    if vals.ndim != 2 or min(vals.shape) < 1:
+        local_err = ValueError("data must be a 2-D matrix with positive dimensions")
+    parallel.agree_on_error(local_err)
+    n0, n_global = parallel.column_offsets(vals.shape[1])
+    F, N = vals.shape
+    fs = parallel.allgather_int(F)
+    if len(set(fs)) != 1:
+        raise ValueError("every rank's column block must have the global row count")
+    ctx = get_context(device, dtype)
+    with ctx.lock:
+        ctx.set_dense(vals, 0.0 if kappa is None else kappa)
+        vmin, _vmax, vsum, nonfinite, count = ctx.data_stats()
+        gmin = float(parallel.allreduce_scalars([vmin], "min")[0])
+        gnf, gsum, gcnt = (float(x) for x in parallel.allreduce_scalars(
+            [nonfinite, vsum, count], "sum"))
+        kappa_in = kappa
+        kappa = _check_global(gmin, gnf, gsum, gcnt, config, kappa)   # same on every rank
+        if kappa_in is None and kappa != 0.0:
+            ctx.set_dense(vals, kappa)
+        local_err = None
+        pair = None
+        try:
+            if init is None:
+                full = init_factors(F, n_global, config.rank, config.seed)
+                init = (full.w, full.h)
+            w0, h0 = init if not isinstance(init, FactorPair) else (init.w, init.h)
+            w0, h0 = parallel.slice_init(w0, h0, n0, N, n_global)
+            pair = _resolve_init((w0, h0), F, N, config.rank, config.seed)
+        except ValueError as e:
+            local_err = e
+        parallel.agree_on_error(local_err)
+        _attach_comm(ctx, n_global)
+        ctx.set_factors(pair.w, pair.h)
+        params = make_params(config, kappa, kkt=kkt, schedule=schedule)
+        done, converged = ctx.run(params, config.max_outer_iters)
+        obj, sec, kk = ctx.trace(done)
+        w, h = ctx.factors()
+    trace = [TraceRow(i + 1, float(obj[i]), float(sec[i]), float(kk[i, 0]), float(kk[i, 1]))
+             for i in range(done)]
+    _count_ops(counter, config, done)
+    return FitResult(factors=_unchecked_pair(w, h), trace=trace,
                      termination=Termination.CONVERGED if converged else Termination.MAX_ITERS,
                      iterations=done, config=config)
 
@@ -440,17 +495,24 @@ def _run_sparse(data, config, counter, algorithm, *, dtype="fp32", init=None, de
         raise ValueError("the sparse path implements one sub-iteration")
     import scipy.sparse as sp
     m = sp.csr_matrix(data, dtype=np.float32)
+    local_err = None
     if not np.isfinite(m.data).all():
-        raise ValueError("data entries must be finite")
-    if m.data.size and m.data.min() < 0.0:
-        raise ValueError("data entries must be nonnegative")
+        local_err = ValueError("data entries must be finite")
+    elif m.data.size and m.data.min() < 0.0:
+        local_err = ValueError("data entries must be nonnegative")
+    elif m.nnz >= 2**31 - 1:
+        local_err = ValueError("the sparse path takes fewer than 2^31 - 1 nonzeros per device")
+    if sharded:
+        from . import parallel
+        if parallel.dist_info() is None:
+            raise ValueError("sharded=True needs an initialised torch.distributed group")
+        parallel.agree_on_error(local_err)   # every rank raises, none waits in a collective
+    elif local_err is not None:
+        raise local_err
     arrays, (F, N) = csr_with_csc_view(m)
     if sharded:
         # `data` is this rank's row block: W rows are local,
         # H is replicated; the init is global (or this rank's W rows)
-        from . import parallel
-        if parallel.dist_info() is None:
-            raise ValueError("sharded=True needs an initialised torch.distributed group")
         f0, f_global = parallel.column_offsets(F)   # offsets of a 1-D partition
         counts = parallel.allgather_int(N)
         if len(set(counts)) != 1:
@@ -465,18 +527,20 @@ def _run_sparse(data, config, counter, algorithm, *, dtype="fp32", init=None, de
         h0 = np.asarray(h0, dtype=np.float64)
         if w0.shape == (f_global, K):
             w0 = w0[f0:f0 + F]
+        local_err = None
         if w0.shape != (F, K) or h0.shape != (K, N):
-            raise ValueError(f"init shapes {w0.shape}, {h0.shape} do not match the global "
-                             f"{(f_global, N)} or local {(F, N)} data at rank {K}")
+            local_err = ValueError(f"init shapes {w0.shape}, {h0.shape} do not match the global "
+                                   f"{(f_global, N)} or local {(F, N)} data at rank {K}")
+        parallel.agree_on_error(local_err)
         w_init, h_init = w0, h0
     else:
         pair = _resolve_init(init, F, N, config.rank, config.seed)
         w_init, h_init = pair.w, pair.h
     ctx = get_context(device, "fp32-sparse")
     with ctx.lock:
+        ctx.set_csr(*arrays, (F, N))   # switches the context to the sparse engine first
         if sharded:
             _attach_comm(ctx, f_global)
-        ctx.set_csr(*arrays, (F, N))
         ctx.set_factors(w_init, h_init)
         params = make_params(config, 0.0, kkt=False, schedule="reference")
         done, converged = ctx.run(params, config.max_outer_iters)

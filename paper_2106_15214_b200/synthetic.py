@@ -115,36 +115,97 @@ def config4(F=256, N=4194304, K=12, seed=4, dtype=np.float64, threads=None,
     return out
 
 
-def config5(F=1000000, N=200000, density=5e-4, seed=5, alpha=1.1):
-    """Sparse counts (CSR): per-row nonzero counts ~ Poisson(density*N), column
-    ids ~ Zipf(alpha) popularity over a seeded column permutation (duplicates
-    within a row merged; one extra entry per row and per column so no row or
-    column is empty), values Geometric(0.3)+1 stored as fp32.
+def _config5_rows(cdf, perm, counts, row_fill, seed, chunk_id):
+    """Column ids of a chunk of rows: Zipf draws without replacement within a
+    row (first occurrences in draw order, the row's fill column drawn first),
+    each row's ids returned sorted.  Returns (per-row counts, flat columns)."""
+    rng = np.random.default_rng([seed, 0xC5, chunk_id])
+    nr = counts.size
+    N = perm.size
+    out = [None] * nr
+    todo = np.arange(nr)
+    mult = 2
+    while todo.size:
+        c = counts[todo]
+        M = int(min(max(c.max() * mult + 16, 32), 64 * N))
+        u = rng.random((todo.size, M))
+        draws = perm[np.minimum(np.searchsorted(cdf, u), N - 1)]
+        draws[:, 0] = row_fill[todo]
+        idx = np.argsort(draws, axis=1, kind="stable")
+        srt = np.take_along_axis(draws, idx, axis=1)
+        first_s = np.ones_like(srt, dtype=bool)
+        first_s[:, 1:] = srt[:, 1:] != srt[:, :-1]
+        first = np.empty_like(first_s)
+        np.put_along_axis(first, idx, first_s, axis=1)
+        cum = np.cumsum(first, axis=1)
+        ok = cum[:, -1] >= c
+        keep = first & (cum <= c[:, None])
+        keep_s = np.take_along_axis(keep, idx, axis=1)
+        for i in np.nonzero(ok)[0]:
+            out[todo[i]] = srt[i][keep_s[i]]
+        todo = todo[~ok]
+        mult *= 2
+    return counts, np.concatenate(out) if out else np.zeros(0, dtype=np.int32)
+
+
+def config5(F=1000000, N=200000, density=5e-4, seed=5, alpha=1.1, threads=None):
+    """Sparse counts (CSR) with exactly round(density * F * N) nonzeros
+    (10^8 at the BASELINE size).
+
+    Per-row nonzero counts ~ Poisson(density * N), rescaled by seeded +-1
+    steps to the exact total; column ids ~ Zipf(alpha) popularity over a
+    seeded column permutation, drawn WITHOUT replacement within a row (a
+    duplicate draw is skipped, so heavy columns saturate instead of merging
+    entries away); every row holds its fill column and every column at least
+    one entry (an all-zero row or column of V drives its factor row/column to
+    exactly 0 under MU, which the reference rejects, majorizer.py:50-51);
+    values Geometric(0.3)+1 stored as fp32.  Rows are generated in seeded
+    chunks, so the result does not depend on the thread count.
 
     Returns (indptr int64, indices int32, data float32, (F, N))."""
     rng = np.random.default_rng(seed)
+    target = int(min(max(round(density * F * N), max(F, N)), F * N))
     ranks = np.arange(1, N + 1, dtype=float)
     p = ranks ** (-alpha)
     cdf = np.cumsum(p / p.sum())
     perm = rng.permutation(N).astype(np.int32)
-    counts = rng.poisson(density * N, size=F)
-    total = int(counts.sum())
-    cols = perm[np.minimum(np.searchsorted(cdf, rng.random(total)), N - 1)]
-    rows = np.repeat(np.arange(F, dtype=np.int64), counts)
-    # every row and every column gets at least one count: an all-zero row or
-    # column of V drives its factor row/column to exactly 0 under MU, which the
-    # reference rejects (majorizer.py:50-51)
-    fill_r = np.arange(F, dtype=np.int64)
-    fill_c = perm[fill_r % N]
-    extra_c = np.arange(N, dtype=np.int32)
-    extra_r = rng.integers(0, F, size=N)
-    rows = np.concatenate([rows, fill_r, extra_r])
-    cols = np.concatenate([cols, fill_c, extra_c])
-    key = rows * N + cols
-    key = np.unique(key)
-    rows = key // N
-    cols = (key % N).astype(np.int32)
-    vals = (rng.geometric(0.3, size=key.size) + 1).astype(np.float32)
+    counts = np.clip(rng.poisson(density * N, size=F), 1, N).astype(np.int64)
+    diff = target - int(counts.sum())
+    while diff != 0:
+        step = np.bincount(rng.integers(0, F, size=abs(diff)), minlength=F)
+        counts += np.minimum(step, N - counts) if diff > 0 else -np.minimum(step, counts - 1)
+        diff = target - int(counts.sum())
+    row_fill = perm[np.arange(F) % N]
+    RCH = 16384
+    chunks = [(a, min(F, a + RCH)) for a in range(0, F, RCH)]
+
+    def work(ci):
+        a, b = chunks[ci]
+        return _config5_rows(cdf, perm, counts[a:b], row_fill[a:b], seed, ci)
+
+    threads = threads or min(8, os.cpu_count() or 1)
+    if len(chunks) == 1 or threads == 1:
+        parts = [work(i) for i in range(len(chunks))]
+    else:
+        with _cf.ThreadPoolExecutor(threads) as ex:
+            parts = list(ex.map(work, range(len(chunks))))
+    cols = np.concatenate([q[1] for q in parts]).astype(np.int32)
     indptr = np.zeros(F + 1, dtype=np.int64)
-    np.cumsum(np.bincount(rows, minlength=F), out=indptr[1:])
+    np.cumsum(counts, out=indptr[1:])
+    # columns left empty: one entry each, replacing an entry of a random row
+    # whose column is held elsewhere too (nnz stays exact)
+    ccount = np.bincount(cols, minlength=N)
+    for j in np.nonzero(ccount == 0)[0]:
+        while True:
+            r = int(rng.integers(0, F))
+            lo, hi = indptr[r], indptr[r + 1]
+            cand = np.nonzero(ccount[cols[lo:hi]] >= 2)[0]
+            if cand.size:
+                pos = lo + int(cand[rng.integers(0, cand.size)])
+                ccount[cols[pos]] -= 1
+                cols[pos] = j
+                ccount[j] += 1
+                cols[lo:hi].sort()
+                break
+    vals = (rng.geometric(0.3, size=cols.size) + 1).astype(np.float32)
     return indptr, cols, vals, (F, N)

@@ -144,3 +144,40 @@ def test_row_sharded_sparse_kl_matches_single_process_oracle():
         for r in res:
             np.testing.assert_allclose(r[3][algo][1], h_ref, rtol=1e-11)   # H replicated
             np.testing.assert_allclose(r[3][algo][2], obj_ref, rtol=1e-12)
+
+
+def _agree_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2106_15214_b200 import parallel
+        parallel.agree_on_error(None)            # nobody failed: no error anywhere
+        err = ValueError("data entries must be finite") if rank == 1 else None
+        try:
+            parallel.agree_on_error(err)
+            q.put((rank, "no error"))
+        except ValueError as e:
+            q.put((rank, str(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_input_errors_agreed_across_ranks():
+    """A check that fails on one rank only raises on every rank (the failing
+    rank its own message), so no rank waits in the next collective (the
+    sharded entries call this before the communicator is created)."""
+    import torch.multiprocessing as mp
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_agree_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[1] == "data entries must be finite"
+    assert res[0] == "input checks failed on rank(s) [1]"

@@ -165,12 +165,15 @@ def kernels():
     print("kernels:", n)
 
 
-def configs():
+def configs(only_sparse=False):
     """BASELINE configs through the reference, fp64, injected U(0,1) init.
 
     fp32 configs are run on the fp32-rounded V (SURVEY.md §8d correctness gates).
+    ``only_sparse`` regenerates just the cfg5p entries (after a change of the
+    config-5 generator) and keeps the rest of configs.npz.
     """
-    out = {}
+    path = os.path.join(HERE, "configs.npz")
+    out = dict(np.load(path)) if only_sparse else {}
     specs = [
         # name, V generator, K, beta, iters, kappa(None=auto), fp32?
         ("cfg1", lambda: synthetic.config1(), 49, 1.0, 200, None, False),
@@ -178,7 +181,7 @@ def configs():
         ("cfg3p", lambda: synthetic.config3(F=1025, N=1024, K=20), 20, 0.0, 60, None, True),
         ("cfg4p", lambda: synthetic.config4(N=4096), 12, 1.5, 60, 0.0, True),
     ]
-    for name, gen, K, beta, iters, kappa, fp32 in specs:
+    for name, gen, K, beta, iters, kappa, fp32 in ([] if only_sparse else specs):
         v = gen()
         if fp32:
             v = v.astype(np.float32).astype(np.float64)
@@ -213,11 +216,14 @@ def configs():
         out[f"cfg5p_{algo}/obj"] = obj
     out["cfg5p/nnz"] = np.array(idx.size)
     out["cfg5p/vsum"] = np.array(float(vals.astype(np.float64).sum()))
-    np.savez_compressed(os.path.join(HERE, "configs.npz"), **out)
+    np.savez_compressed(path, **out)
     print("configs written")
 
 
 if __name__ == "__main__":
-    fits()
-    kernels()
-    configs()
+    if sys.argv[1:] == ["cfg5p"]:
+        configs(only_sparse=True)
+    else:
+        fits()
+        kernels()
+        configs()

@@ -171,6 +171,34 @@ def test_sparse_matches_oracle_restatement_and_is_deterministic():
     assert max_rel(got, obj) <= 1e-4
 
 
+def test_sparse_heavy_columns_and_row_tiles_match_oracle():
+    """The sparse code paths that only exist at scale, against the oracle restatement: 300 000
+    rows span three SP_TILE = 131072 row tiles, and under Zipf(1.1) over 1500 columns the
+    heaviest columns hold > 100 000 nonzeros each -- far above SP_HEAVY = 2048 (row-tiled
+    512-nonzero segments) and above SP_B2_HEAVY = 64 segments (pass B2h, one block per
+    column).  25 iterations, JMM and BMM, north-star fp32 gate."""
+    import scipy.sparse as sp
+    from oracle import betanmf_oracle as O
+    from paper_2106_15214_b200 import synthetic
+    indptr, idx, vals, shape = synthetic.config5(F=300000, N=1500, density=0.004, seed=77)
+    counts = np.bincount(idx, minlength=shape[1])
+    assert counts.max() > 64 * 512 and (counts > 2048).sum() >= 20
+    assert shape[0] > 2 * 131072
+    csr = sp.csr_matrix((vals, idx, indptr), shape=shape)
+    w0, h0 = synthetic.uniform_init(shape[0], shape[1], 16, seed=116)
+    for algo in ("jmm", "bmm"):
+        cfg = bn.SolverConfig(beta=1.0, rank=16, algorithm=algo, kappa=0.0, tol=1e-300,
+                              max_outer_iters=25)
+        res = bn.fit(csr, cfg, init=(w0, h0), dtype="fp32")
+        wr, hr, obj, _ = O.run_sparse_kl(csr.astype(np.float64), 16, algo, max_outer_iters=25,
+                                         init=(w0, h0))
+        got = np.array([t.objective for t in res.trace])
+        assert max_rel(got, obj) <= 1e-4, (algo, max_rel(got, obj))
+        assert np.all(got[1:] <= got[:-1] * (1 + 1e-6))
+        assert np.linalg.norm(res.factors.w - wr) / np.linalg.norm(wr) <= 1e-3
+        assert np.linalg.norm(res.factors.h - hr) / np.linalg.norm(hr) <= 1e-3
+
+
 def test_sparse_sharded_entry_with_one_rank_matches_unsharded():
     """The row-sharded sparse entry (sharded=True: global init sliced by row
     offsets, NCCL communicator attached) on a 1-rank process group gives the
@@ -197,6 +225,40 @@ def test_sparse_sharded_entry_with_one_rank_matches_unsharded():
     dist.init_process_group("gloo", rank=0, world_size=1)
     try:
         got = bn.fit(csr, cfg, init=(w0, h0), dtype="fp32", sharded=True)
+    finally:
+        dist.destroy_process_group()
+    assert [t.objective for t in got.trace] == [t.objective for t in ref.trace]
+    assert np.array_equal(got.factors.w, ref.factors.w)
+    assert np.array_equal(got.factors.h, ref.factors.h)
+
+
+@pytest.mark.parametrize("dtype,shape", [("fp32", (256, 4100, 12, 1.5)), ("fp32", (300, 2000, 20, 0.0)),
+                                         ("fp64", (64, 500, 5, 1.0))])
+def test_dense_sharded_entry_with_one_rank_matches_unsharded(dtype, shape):
+    """Dense fit(..., sharded=True) (N-column shard) on a 1-rank process group:
+    the communicator is attached (ncclCommInitRank with nranks = 1), the global checks run on
+    allreduced device statistics, the init is sliced by column offsets -- and the result is
+    bitwise the unsharded one (tcgen05 pass, SIMT pair and the fp64 reference schedule)."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+    F, N, K, beta = shape
+    v = bn.synthetic_low_rank(F, N, K, noise=0.05, seed=F + N)
+    if dtype == "fp32":
+        v = v.astype(np.float32)
+    init = bn.init_factors(F, N, K, seed=K)
+    cfg = bn.SolverConfig(beta=beta, rank=K, algorithm="jmm", tol=1e-300, max_outer_iters=15)
+    ref = bn.fit(v, cfg, init=init, dtype=dtype, kkt=False)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        got = bn.fit(v, cfg, init=(init.w, init.h), dtype=dtype, kkt=False, sharded=True)
     finally:
         dist.destroy_process_group()
     assert [t.objective for t in got.trace] == [t.objective for t in ref.trace]

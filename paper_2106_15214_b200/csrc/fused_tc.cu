@@ -23,6 +23,7 @@
 #include "fused_simt.cuh"
 #include "fused_simt2.cuh"
 #include "fused_tc_kernel.cuh"
+#include "fused_tc2_kernel.cuh"
 #include "small_kernels.cuh"
 
 namespace bnmf {
@@ -50,7 +51,16 @@ struct FusedState {
   CUtensorMap mapV;
   long long* prof = nullptr;   // BNMF_TC_PROF=1: wait-cycle counters [grid][48]
   int cap = 0;                 // BNMF_TC_MAX_CLUSTERS at creation (test knob)
+  bool v1 = true;              // false with BNMF_TC_V2=1 (second-generation kernel, A/B knob)
 };
+
+// BNMF_TC_V2=1 selects the second-generation kernel (fused_tc2_kernel.cuh: item teams, two
+// issuing warps, a dedicated U team).  It is parity-green but measured slower than the first
+// generation on config 4 (profiles/r02_fused_pass_experiments.md), so v1 stays the default.
+static bool env_tc_v1() {
+  const char* c = getenv("BNMF_TC_V2");
+  return !(c && c[0] == '1');
+}
 
 static int env_cluster_cap() {
   const char* c = getenv("BNMF_TC_MAX_CLUSTERS");
@@ -85,7 +95,7 @@ static cudaLaunchConfig_t tc_config(const FusedState* fs, cudaStream_t stream,
                                     cudaLaunchAttribute* attr) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(fs->tc_grid, 1, 1);
-  cfg.blockDim = dim3(ftc::NTHREADS, 1, 1);
+  cfg.blockDim = dim3(fs->v1 ? ftc::NTHREADS : ftc2::NTHREADS2, 1, 1);
   cfg.dynamicSmemBytes = fs->tc_smem;
   cfg.stream = stream;
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -189,7 +199,8 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
       fs->tc_cl = 1;
       fs->tc_f0 = io.F;
     }
-    auto kern = ftc::fused_pass_tc<ftc::FBC_15, false>;
+    fs->v1 = env_tc_v1();
+    auto kern = fs->v1 ? ftc::fused_pass_tc<ftc::FBC_15, false> : ftc2::fused_pass_tc2<ftc::FBC_15, false>;
     FCK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fs->tc_smem)));
     FCK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     int clusters = nsm / fs->tc_cl;
@@ -213,7 +224,7 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
   const int gobj = std::max(gmax, fs->s2_S * fs->s2_rc);
   const char* prof_env = getenv("BNMF_TC_PROF");
   if (fs->tc && prof_env && prof_env[0] == '1') {
-    const size_t np = size_t(fs->tc_grid) * 48 + 3 * 4096;
+    const size_t np = size_t(fs->tc_grid) * 288 + 3 * 4096;
     FCK(cudaMalloc(&fs->prof, np * sizeof(long long)));
     FCK(cudaMemset(fs->prof, 0, np * sizeof(long long)));
     g_last_tc = fs;
@@ -295,7 +306,7 @@ static cudaError_t launch_simt(FusedState* fs, const FusedArgs& a, const FusedIO
 template <int FBC, bool KAPPA>
 static cudaError_t launch_tc(FusedState* fs, const FusedArgs& a, const FusedIO& io, int slot,
                              int p_override) {
-  auto kern = ftc::fused_pass_tc<FBC, KAPPA>;
+  auto kern = fs->v1 ? ftc::fused_pass_tc<FBC, KAPPA> : ftc2::fused_pass_tc2<FBC, KAPPA>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fs->tc_smem));
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchAttribute attr[1];
@@ -368,7 +379,7 @@ static int enqueue_pass_and_update(FusedState* fs, const FusedIO& io, int slot, 
 }
 
 bool fused_shape_matches(const FusedState* fs, int F, int N, int K) {
-  return fs && fs->F == F && fs->N == N && fs->K == K && (!fs->tc || fs->cap == env_cluster_cap());
+  return fs && fs->F == F && fs->N == N && fs->K == K && (!fs->tc || (fs->cap == env_cluster_cap() && fs->v1 == env_tc_v1()));
 }
 
 void fused_info(const FusedState* fs, int* out4) {
@@ -440,7 +451,7 @@ int fused_export(FusedState* fs, const FusedIO& io, std::string& err) {
 extern "C" int bnmf_tc_prof_read(long long* out, int max) {
   bnmf::FusedState* fs = bnmf::g_last_tc;
   if (!fs || !fs->prof) return 0;
-  int n = std::min(max, fs->tc_grid * 48 + 3 * 4096);
+  int n = std::min(max, fs->tc_grid * 288 + 3 * 4096);
   if (cudaMemcpy(out, fs->prof, size_t(n) * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
     return -1;
   return n;

@@ -64,6 +64,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// the same by 32-bit shared address (callers that keep barrier addresses in registers)
+__device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
+#ifdef BNMF_WATCHDOG
+  const long long t0 = clock64();
+  while (!mbar_try(a, parity)) {
+    if (clock64() - t0 > (1ll << 32)) {
+      printf("bnmf watchdog: block %d thread %d stuck on mbarrier %u parity %u\n", blockIdx.x,
+             threadIdx.x, a, parity);
+      __trap();
+    }
+  }
+#else
+  while (!mbar_try(a, parity)) {
+  }
+#endif
+}
+__device__ __forceinline__ void mbar_arrive_a(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+
 // ---- TMA ------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
@@ -382,6 +402,7 @@ __device__ __forceinline__ uint64_t f2sub(uint64_t a, uint64_t b) {
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+__device__ __forceinline__ uint64_t f2neg(uint64_t a) { return a ^ 0x8000000080000000ull; }
 __device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
   uint64_t r;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));

@@ -627,12 +627,9 @@ struct Engine : EngineBase {
     if (fused_active) {
       FusedIO o = io();
       if (prof && slot < kChunk) { o.ev_a = ev_a[slot]; o.ev_b = ev_b[slot]; prof_slots = std::max(prof_slots, slot + 1); }
+      // KKT residuals (p.compute_kkt) are part of the fused slot: res_W from the reduced
+      // W-side sums, res_H from an H-side-only pass (fused_tc.cu, enqueue_kkt)
       if (fused_enqueue_iteration(fused, o, slot, err)) return fail(BNMF_E_CUDA, err);
-      if (p.compute_kkt) {
-        // the KKT passes read the normalised iterate from the standard buffers
-        if (fused_select(fused, o, err)) return fail(BNMF_E_CUDA, err);
-        return enqueue_kkt(slot);
-      }
       return 0;
     }
     return enqueue_reference_iteration(slot);

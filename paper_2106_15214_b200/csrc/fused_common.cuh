@@ -35,6 +35,8 @@ struct FusedArgs {
   int algorithm;          // 0 jmm, 1 bmm
   int do_h;               // 0 = prologue (W-side + objective only)
   int den_ones;           // beta == 1: H den = colsum(C2), W den = rowsum(H~)
+  int kkt;                // 1 = KKT pass (H side only, no update): sum |min(H~_p, W~_p^T (Zd - Zn))|
+                          // per CTA into opart (diagnostics.py:46-59); Wa = C1 = C2 = W~_p
   long long* prof;        // optional per-CTA wait-cycle counters [G][48] (BNMF_TC_PROF=1)
   Scalars sc;
 };

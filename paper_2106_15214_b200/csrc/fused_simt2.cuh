@@ -220,9 +220,15 @@ hpass(FusedArgs a, const RunState* st, int slot, int p_override) {
   float* Zn = B0 + 2 * bsz;                         // [TF][NC]
   float* Zd = Zn + TF * NC;
   const int par = iter_parity(st, slot, p_override);
-  const float* Hprev = a.Hbuf[par ^ 1];
+  // KKT pass (a.kkt): the same sums on the finished iterate (W~_p, H~_p) with W~_p as both
+  // chi maps give W~^T Zn and W~^T Zd; the block reports sum |min(H~_p, den - num)|
+  // (diagnostics.py:55-58) instead of updating H
+  const int kkt = a.kkt;
+  const float* Hprev = kkt ? a.Hbuf[par] : a.Hbuf[par ^ 1];
   float* Hnew = a.Hout[par];
-  const float* Wa = a.algorithm == 0 ? a.Wt2[par ^ 1] : a.Wn;
+  const float* Wa = kkt ? a.Wt2[par] : (a.algorithm == 0 ? a.Wt2[par ^ 1] : a.Wn);
+  const float* C1g = kkt ? a.Wt2[par] : a.C1;
+  const float* C2g = kkt ? a.Wt2[par] : a.C2;
   const float kappa = float(a.sc.kappa), beta = float(a.sc.beta);
   const int tid = threadIdx.x, tn = tid & 15, tf = tid >> 4;
   const int n0 = blockIdx.x * NC;
@@ -254,12 +260,12 @@ hpass(FusedArgs a, const RunState* st, int slot, int p_override) {
     float* c1 = ws + TF * rs;
     if (k16) {
       rows_async16(ws, Wa + (size_t)f0 * K, TF, vf, K, rs, rmap);
-      rows_async16(c1, a.C1 + (size_t)f0 * K, TF, vf, K, KS, rmap);
-      if (DEN) rows_async16(c1 + TF * KS, a.C2 + (size_t)f0 * K, TF, vf, K, KS, rmap);
+      rows_async16(c1, C1g + (size_t)f0 * K, TF, vf, K, KS, rmap);
+      if (DEN) rows_async16(c1 + TF * KS, C2g + (size_t)f0 * K, TF, vf, K, KS, rmap);
     } else {
       tile_async(ws, Wa + (size_t)f0 * K, TF, vf, K, rs, kr);
-      tile_async(c1, a.C1 + (size_t)f0 * K, TF, vf, K, KS, KS);
-      if (DEN) tile_async(c1 + TF * KS, a.C2 + (size_t)f0 * K, TF, vf, K, KS, KS);
+      tile_async(c1, C1g + (size_t)f0 * K, TF, vf, K, KS, KS);
+      if (DEN) tile_async(c1 + TF * KS, C2g + (size_t)f0 * K, TF, vf, K, KS, KS);
     }
     vtile_async(c1 + 2 * TF * KS, a.V + (size_t)f0 * a.ldv + n0, a.ldv, vf, valid_n);
     cp_commit();
@@ -358,6 +364,29 @@ hpass(FusedArgs a, const RunState* st, int slot, int p_override) {
       accn[m] += double(tn_);
       if (DEN) accd[m] += double(td_);
     }
+  }
+  if (kkt) {
+    // res_H partial of this column block (a.csum2 = colsum(W~_p) when beta = 1)
+    double t = 0.0;
+#pragma unroll
+    for (int m = 0; m < NOUT; ++m) {
+      const int e = tid + THREADS * m, k = e / NC, n = e - k * NC;
+      if (k < K && n < valid_n) {
+        const double den = DEN ? accd[m] : a.csum2[k];
+        t += fabs(fmin(double(Hp[n * rs + k]), den - accn[m]));
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    __syncthreads();
+    double* redd = reinterpret_cast<double*>(Red);
+    if ((tid & 31) == 0) redd[tid >> 5] = t;
+    __syncthreads();
+    if (tid == 0) {
+      double tt = 0.0;
+      for (int w = 0; w < THREADS / 32; ++w) tt += redd[w];
+      a.opart[blockIdx.x] = tt;
+    }
+    return;
   }
   // H_p = H~_{p-1} * ratio^gamma ; H~_p = H_p * norms_p
 #pragma unroll

@@ -52,6 +52,9 @@ struct FusedState {
   long long* prof = nullptr;   // BNMF_TC_PROF=1: wait-cycle counters [grid][48]
   int cap = 0;                 // BNMF_TC_MAX_CLUSTERS at creation (test knob)
   bool v1 = true;              // false with BNMF_TC_V2=1 (second-generation kernel, A/B knob)
+  double* kpart = nullptr;     // KKT pass: per-CTA sums of |min(H~, grad_H)|
+  int kparts = 0;
+  double* kcs = nullptr;       // KKT pass, beta = 1 on the SIMT pair: colsum(W~_p) (K)
 };
 
 // BNMF_TC_V2=1 selects the second-generation kernel (fused_tc2_kernel.cuh: item teams, two
@@ -92,10 +95,10 @@ bool fused_tc_shape_ok(int F, int K) {
 
 template <int FBC, bool KAPPA>
 static cudaLaunchConfig_t tc_config(const FusedState* fs, cudaStream_t stream,
-                                    cudaLaunchAttribute* attr) {
+                                    cudaLaunchAttribute* attr, bool v2) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(fs->tc_grid, 1, 1);
-  cfg.blockDim = dim3(fs->v1 ? ftc::NTHREADS : ftc2::NTHREADS2, 1, 1);
+  cfg.blockDim = dim3(v2 ? ftc2::NTHREADS2 : ftc::NTHREADS, 1, 1);
   cfg.dynamicSmemBytes = fs->tc_smem;
   cfg.stream = stream;
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -208,7 +211,7 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
       cudaLaunchAttribute attr[1];
       FusedState probe = *fs;
       probe.tc_grid = fs->tc_cl * clusters;
-      cudaLaunchConfig_t cfg = tc_config<ftc::FBC_15, false>(&probe, io.stream, attr);
+      cudaLaunchConfig_t cfg = tc_config<ftc::FBC_15, false>(&probe, io.stream, attr, !fs->v1);
       int maxc = 0;
       if (cudaOccupancyMaxActiveClusters(&maxc, kern, &cfg) == cudaSuccess && maxc > 0)
         clusters = std::min(clusters, maxc);
@@ -229,6 +232,9 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
     FCK(cudaMemset(fs->prof, 0, np * sizeof(long long)));
     g_last_tc = fs;
   }
+  fs->kparts = std::max(gmax, (io.N + fs2::NC - 1) / fs2::NC);
+  FCK(cudaMalloc(&fs->kpart, size_t(fs->kparts) * sizeof(double)));
+  FCK(cudaMalloc(&fs->kcs, io.K * sizeof(double)));
   FCK(cudaMalloc(&fs->part, size_t(gmax) * 2 * fk * sizeof(double)));
   FCK(cudaMalloc(&fs->opart, size_t(gobj) * sizeof(double)));
   if (fs->tc) {
@@ -253,7 +259,7 @@ void fused_destroy(FusedState* fs) {
   if (!fs) return;
   float* fp[] = {fs->H[0], fs->H[1], fs->W2[0], fs->W2[1], fs->Wn, fs->C1, fs->C2};
   for (float* q : fp) if (q) cudaFree(q);
-  double* dp[] = {fs->norms, fs->csum2, fs->part, fs->opart};
+  double* dp[] = {fs->norms, fs->csum2, fs->part, fs->opart, fs->kpart, fs->kcs};
   for (double* q : dp) if (q) cudaFree(q);
   if (fs->prof) cudaFree(fs->prof);
   if (g_last_tc == fs) g_last_tc = nullptr;
@@ -275,6 +281,7 @@ static FusedArgs make_args(FusedState* fs, const FusedIO& io, int do_h) {
   a.den_ones = beta_class(io.sc.beta) == BC_1 ? 1 : 0;
   a.sc = io.sc;
   a.prof = fs->prof;
+  a.kkt = 0;
   return a;
 }
 
@@ -288,6 +295,7 @@ static cudaError_t launch_simt2(FusedState* fs, const FusedArgs& a, const FusedI
     hk<<<(io.N + fs2::NC - 1) / fs2::NC, fs2::THREADS, hs, io.stream>>>(a, io.st, slot,
                                                                           p_override);
   }
+  if (a.kkt) return cudaGetLastError();
   auto wk = fs2::wpass<BC, KJ>;
   const int ws = int(fs2::w_smem(io.K));
   cudaFuncSetAttribute(wk, cudaFuncAttributeMaxDynamicSharedMemorySize, ws);
@@ -306,11 +314,13 @@ static cudaError_t launch_simt(FusedState* fs, const FusedArgs& a, const FusedIO
 template <int FBC, bool KAPPA>
 static cudaError_t launch_tc(FusedState* fs, const FusedArgs& a, const FusedIO& io, int slot,
                              int p_override) {
-  auto kern = fs->v1 ? ftc::fused_pass_tc<FBC, KAPPA> : ftc2::fused_pass_tc2<FBC, KAPPA>;
+  // the KKT pass exists in the second-generation kernel only
+  const bool v2 = !fs->v1 || a.kkt;
+  auto kern = v2 ? ftc2::fused_pass_tc2<FBC, KAPPA> : ftc::fused_pass_tc<FBC, KAPPA>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(fs->tc_smem));
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchAttribute attr[1];
-  cudaLaunchConfig_t cfg = tc_config<FBC, KAPPA>(fs, io.stream, attr);
+  cudaLaunchConfig_t cfg = tc_config<FBC, KAPPA>(fs, io.stream, attr, v2);
   return cudaLaunchKernelEx(&cfg, kern, a, fs->mapV, fs->tc_cl, fs->tc_f0, io.st, slot,
                             p_override);
 }
@@ -378,6 +388,105 @@ static int enqueue_pass_and_update(FusedState* fs, const FusedIO& io, int slot, 
   return 0;
 }
 
+// ---- KKT residuals of the finished iterate (diagnostics.py:46-59), untimed like the
+// reference's (they follow finish_iter) ---------------------------------------------------------
+//   res_W: grad_W = Zd H~^T - Zn H~^T at (W~_p, H~_p) are the W-side sums pass p has just
+//          reduced into comm for iteration p+1, so it costs F K operations
+//   res_H: one H-side-only pass (tcgen05: fused_pass_tc2 in KKT mode; else fs2::hpass in KKT
+//          mode) with W~_p as both chi maps; per-CTA partials in kpart
+static __global__ void kkt_colsum(WPair Wt2, int F, int K, double* out, const RunState* st,
+                                  int slot) {
+  if (!iter_active(st, slot)) return;
+  const float* W = Wt2.w[iter_parity(st, slot, -1)];
+  const int k = blockIdx.x;
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int f = threadIdx.x; f < F; f += blockDim.x) s += double(W[size_t(f) * K + k]);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < int(blockDim.x + 31) / 32; ++w) t += red[w];
+    out[k] = t;
+  }
+}
+
+// comm[2FK + 1] = sum of the per-CTA res_H partials (fixed order: strided per thread, then a tree)
+static __global__ void __launch_bounds__(1024) kkt_sum(const double* __restrict__ kpart, int G,
+                                                       double* __restrict__ out,
+                                                       const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  __shared__ double red[1024];
+  double s = 0.0;
+  for (int g = threadIdx.x; g < G; g += 1024) s += kpart[g];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+static __global__ void __launch_bounds__(1024) kkt_finish(const double* __restrict__ comm, WPair Wt2,
+                                                          int F, int K, double kn,
+                                                          double* __restrict__ tr_kkt,
+                                                          const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  const float* W = Wt2.w[iter_parity(st, slot, -1)];
+  const size_t fk = size_t(F) * K;
+  __shared__ double red[32];
+  double s = 0.0;
+  for (size_t i = threadIdx.x; i < fk; i += blockDim.x)
+    s += fabs(fmin(double(W[i]), comm[fk + i] - comm[i]));
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 32; ++w) t += red[w];
+    const long long it = st->base + slot;
+    tr_kkt[2 * (it - 1) + 0] = t / double(fk);
+    tr_kkt[2 * (it - 1) + 1] = comm[2 * fk + 1] / kn;
+  }
+}
+
+static int enqueue_kkt(FusedState* fs, const FusedIO& io, int slot, std::string& err) {
+  FusedArgs a = make_args(fs, io, 1);
+  a.kkt = 1;
+  a.opart = fs->kpart;
+  a.csum2 = fs->kcs;
+  WPair wp;
+  wp.w[0] = fs->W2[0]; wp.w[1] = fs->W2[1];
+  const size_t fk2 = size_t(2) * io.F * io.K;
+  int nparts = fs->tc_grid;
+  if (!fs->tc) {
+    nparts = (io.N + fs2::NC - 1) / fs2::NC;
+    if (a.den_ones) {
+      kkt_colsum<<<io.K, 256, 0, io.stream>>>(wp, io.F, io.K, fs->kcs, io.st, slot);
+      FCK(cudaGetLastError());
+      if (io.launches) *io.launches += 1;
+    }
+  }
+  FCK(launch_pass(fs, a, io, slot, -1));
+  kkt_sum<<<1, 1024, 0, io.stream>>>(fs->kpart, nparts, io.comm + fk2 + 1, io.st, slot);
+  FCK(cudaGetLastError());
+  if (io.launches) *io.launches += 2;
+  if (io.nranks > 1) {
+    ncclResult_t r = ncclAllReduce(io.comm + fk2 + 1, io.comm + fk2 + 1, 1, ncclDouble, ncclSum,
+                                   io.nccl, io.stream);
+    if (r != ncclSuccess) { err = std::string("ncclAllReduce: ") + ncclGetErrorString(r); return -1; }
+    if (io.launches) *io.launches += 1;
+  }
+  kkt_finish<<<1, 1024, 0, io.stream>>>(io.comm, wp, io.F, io.K,
+                                        double(io.K) * double(io.nranks > 1 ? io.n_global : io.N),
+                                        io.tr_kkt, io.st, slot);
+  FCK(cudaGetLastError());
+  if (io.launches) *io.launches += 1;
+  return 0;
+}
+
 bool fused_shape_matches(const FusedState* fs, int F, int N, int K) {
   return fs && fs->F == F && fs->N == N && fs->K == K && (!fs->tc || (fs->cap == env_cluster_cap() && fs->v1 == env_tc_v1()));
 }
@@ -409,7 +518,9 @@ int fused_enqueue_iteration(FusedState* fs, const FusedIO& io, int slot, std::st
   begin_iter<<<1, 1, 0, io.stream>>>(io.st, slot);
   FCK(cudaGetLastError());
   if (io.launches) *io.launches += 1;
-  return enqueue_pass_and_update(fs, io, slot, -1, true, err);
+  if (int rc = enqueue_pass_and_update(fs, io, slot, -1, true, err)) return rc;
+  if (io.compute_kkt) return enqueue_kkt(fs, io, slot, err);
+  return 0;
 }
 
 // Copy the iterate of parity(iters_done) into the engine's Wt / Ht.

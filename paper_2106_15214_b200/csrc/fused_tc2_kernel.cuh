@@ -102,6 +102,7 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 40);
   __shared__ double s_red[NTEAM * TEAM_WARPS];
   __shared__ float s_nrm[KP], s_cs2[KP];
+  __shared__ double s_redu[U_WARPS];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // optional wait-cycle counters (build with BNMF_TC_PROF=1): lane 0 of every warp
@@ -145,11 +146,17 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
   const int nb = pi < nblocks ? (nblocks - 1 - pi) / npairs + 1 : 0;
   const int par = iter_parity(st, slot, p_override);
   const int do_h = a.do_h;
-  const float* Hprev = do_h ? a.Hbuf[par ^ 1] : a.Hbuf[par];
+  // KKT pass: the H items run on the finished iterate (W~_p, H~_p) with W~_p as both chi
+  // maps, so AccH holds W~^T Zn and W~^T Zd; no W items, no update, no publish
+  const int kkt = a.kkt;
+  const float* Hprev = (do_h && !kkt) ? a.Hbuf[par ^ 1] : a.Hbuf[par];
   float* Hnew = a.Hout[par];
   const float* Wt = a.Wt2[par];
-  const float* Wa = a.algorithm == 0 ? a.Wt2[par ^ 1] : a.Wn;
-  const int den_ones = a.den_ones;
+  const float* Wa = kkt ? Wt : (a.algorithm == 0 ? a.Wt2[par ^ 1] : a.Wn);
+  const float* C1g = kkt ? Wt : a.C1;
+  const float* C2g = kkt ? Wt : a.C2;
+  const int den_ones = kkt ? 0 : a.den_ones;
+  const int n_w = kkt ? 0 : SW;   // W items per block
   const float kappa = float(a.sc.kappa), beta = float(a.sc.beta);
   auto col0 = [&](int blk) { return (pi + blk * npairs) * BN; };
 
@@ -190,10 +197,10 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
       v = ok ? Wa[gi] : 0.f; hi = tf32_hi(v);
       sts_f32(sb + OFF_WA + core_off(fl, k), hi);
       sts_f32(sb + OFF_WA + HILO + core_off(fl, k), v - hi);
-      v = ok ? a.C1[gi] : 0.f; hi = tf32_hi(v);
+      v = ok ? C1g[gi] : 0.f; hi = tf32_hi(v);
       sts_f32(sb + OFF_C1 + coreT_off(k, fl), hi);
       sts_f32(sb + OFF_C1 + coreT_off(k + 16, fl), v - hi);
-      v = ok ? a.C2[gi] : 0.f; hi = tf32_hi(v);
+      v = ok ? C2g[gi] : 0.f; hi = tf32_hi(v);
       sts_f32(sb + OFF_C2 + coreT_off(k, fl), hi);
       sts_f32(sb + OFF_C2 + coreT_off(k + 16, fl), v - hi);
     }
@@ -250,8 +257,8 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
     };
     for (int bi = 0; bi < nb; ++bi) {
       if (do_h) {
-        const int j0 = bi == 0 ? 0 : 2;
-        const int n_own = SH - j0, n_all = n_own + (bi + 1 < nb ? 2 : 0);
+        const int j0 = (bi == 0 || kkt) ? 0 : 2;
+        const int n_own = SH - j0, n_all = n_own + ((bi + 1 < nb && !kkt) ? 2 : 0);
         for (int t = 0; t < n_all; ++t) {
           const bool own = t < n_own;
           const int j = own ? j0 + t : t - n_own;
@@ -259,8 +266,8 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
           vt(true, j, j == SH - 1);
         }
       }
-      PWAIT(bar_hn, bi & 1, 1);
-      for (int u = 0; u < SW; ++u) vt(false, u, false);
+      if (n_w) PWAIT(bar_hn, bi & 1, 1);
+      for (int u = 0; u < n_w; ++u) vt(false, u, false);
     }
   } else if (warp == W_SIDE) {
     // ======================= side issuer =====================================
@@ -289,15 +296,15 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
     };
     for (int bi = 0; bi < nb; ++bi) {
       if (do_h) {
-        const int j0 = bi == 0 ? 0 : 2;
-        const int n_own = SH - j0, n_all = n_own + (bi + 1 < nb ? 2 : 0);
+        const int j0 = (bi == 0 || kkt) ? 0 : 2;
+        const int n_own = SH - j0, n_all = n_own + ((bi + 1 < nb && !kkt) ? 2 : 0);
         for (int t = 0; t < n_all; ++t) {
           const bool own = t < n_own;
           side_h(own ? bi : bi + 1, own ? j0 + t : t - n_own);
         }
       }
       const bool fold_end = (bi % FOLD) == FOLD - 1 || bi == nb - 1;
-      for (int u = 0; u < SW; ++u) {
+      for (int u = 0; u < n_w; ++u) {
         const int b = c & 1, m = c >> 1;
         ++c;
         const uint32_t zb = tmem + TM_Z + 128 * b;
@@ -485,8 +492,8 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
       p_nxt = p_cur;
       if (s_nxt >= NSTAGE) { s_nxt -= NSTAGE; p_nxt ^= 1u; }
       if (do_h) {
-        const int j0 = bi == 0 ? 0 : 2;
-        const int n_own = SH - j0, n_all = n_own + (bi + 1 < nb ? 2 : 0);
+        const int j0 = (bi == 0 || kkt) ? 0 : 2;
+        const int n_own = SH - j0, n_all = n_own + ((bi + 1 < nb && !kkt) ? 2 : 0);
         for (int t = 0; t < n_all; ++t) {
           const bool mine = (c & 1) == team;
           ++c;
@@ -501,14 +508,14 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
       }
       // this warp's V rows of the block are stage q
       uint32_t xrow = 0;
-      if (q < SH) {
+      if (q < SH && n_w) {
         uint32_t ph;
         const int s = slot_of(s_cur, p_cur, q, ph);
         PWAITA(full_a + 8 * s, ph, 3);
         xrow = sb + OFF_STAGE + s * STAGE_BYTES + lane * VROWB;
       }
       const int n0 = col0(bi);
-      for (int u = 0; u < SW; ++u) {
+      for (int u = 0; u < n_w; ++u) {
         const bool mine = (c & 1) == team;
         ++c;
         if (mine) w_item(n0, u, xrow);
@@ -589,6 +596,7 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
     if (do_h && nb > 0) write_hp(h0);
     else tc_fence_before();
     int nfold = 0;
+    double kres = 0.0;
     for (int bi = 0; bi < nb; ++bi) {
       const int n = col0(bi) + row;
       float hv[KP];
@@ -663,6 +671,21 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
           __syncwarp();
           if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(bar_xempty), peer));
           PTIME_END(t_chain, 10);
+        }
+        if (kkt) {
+          // res_H partial: |min(H~_p, W~_p^T Zd - W~_p^T Zn)| (diagnostics.py:55-58); each
+          // column is counted by one CTA of the pair
+          if ((CL == 1 || (q >> 1) == int(rank)) && n < N) {
+            float t = 0.f;
+#pragma unroll
+            for (int k = 0; k < KP; ++k)
+              if (k < K) t += fabsf(fminf(h0[k], uden[k] - unum[k]));
+            kres += double(t);
+          }
+#pragma unroll
+          for (int k = 0; k < KP; ++k) h0[k] = h1[k];
+          load_rows(bi + 2, h1);
+          continue;
         }
         // H~_p = H~_{p-1} (num / max(den, floor))^gamma norms; k >= K has h0 = nrm = 0
         float r[KP];
@@ -767,7 +790,10 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
         ++nfold;
       }
     }
-    if (nfold == 0 && row < FTr) {   // CTA without blocks: zero its slab rows
+    if (kkt) {
+      for (int o = 16; o > 0; o >>= 1) kres += __shfl_down_sync(0xffffffffu, kres, o);
+      if (lane == 0) s_redu[warp - W_UTEAM] = kres;
+    } else if (nfold == 0 && row < FTr) {   // CTA without blocks: zero its slab rows
       for (int s = 0; s < 2; ++s)
         for (int k = 0; k < K; ++k) mypart[size_t(s) * F * K + size_t(row0 + row) * K + k] = 0.0;
     }
@@ -792,6 +818,10 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int i = 0; i < NTEAM * TEAM_WARPS; ++i) t += s_red[i];
+    if (kkt) {
+      t = 0.0;
+      for (int i = 0; i < U_WARPS; ++i) t += s_redu[i];
+    }
     a.opart[blockIdx.x] = t;
   }
   if (CL > 1) cluster_sync_all();   // no CTA leaves while its peer may still signal it

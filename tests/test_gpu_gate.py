@@ -97,3 +97,31 @@ def test_second_generation_kernel_200_iterations(name, cap):
     """BNMF_TC_V2=1 (fused_tc2_kernel.cuh: item teams, two issuing warps, U team) holds the
     same gate; it is opt-in because it measured slower (profiles/r02_fused_pass_experiments.md)."""
     _run_case(name, cap=cap, expect_tc=True, v2=True)
+
+
+@pytest.mark.parametrize("name", ["cfg4s", "cfg4b", "cfg4k", "cfg2", "cfg3"])
+def test_fused_kkt_residuals_match_reference(name):
+    """KKT residuals of the fused schedule (kkt=True, the fit() default): res_W from the W-side
+    sums the pass has reduced anyway, res_H from the H-side-only KKT pass, against the
+    reference's trace (diagnostics.py:46-59) over 60 iterations.  fp32 forms the gradients as
+    differences of sums (den - num), so the tolerance is 2e-3 relative plus 1e-6 of the first
+    residual."""
+    z = load_golden("gate.npz")
+    gen, K, beta, kappa = CASES[name]
+    v = gen().astype(np.float32)
+    F, N = v.shape
+    w0, h0 = syn.uniform_init(F, N, K, seed=100 + K)
+    its = 60
+    for algo in ("jmm", "bmm"):
+        ref = z[f"{name}_{algo}/kkt"][:its]
+        ref_obj = z[f"{name}_{algo}/obj"][:its]
+        cfg = bn.SolverConfig(beta=beta, rank=K, algorithm=algo, tol=1e-300, kappa=kappa,
+                              max_outer_iters=its)
+        res = bn.fit(v, cfg, init=(w0, h0), dtype="fp32")
+        assert bn.get_context(0, "fp32").schedule() == "fused"
+        got = np.array([[r.kkt_w, r.kkt_h] for r in res.trace])
+        obj = np.array([r.objective for r in res.trace])
+        assert max_rel(obj, ref_obj) <= 1e-4
+        assert np.all(np.isfinite(got))
+        err = np.abs(got - ref) / (np.abs(ref) + 1e-6 * np.abs(ref[0]))
+        assert err.max() <= 2e-3, (name, algo, float(err.max()), np.unravel_index(err.argmax(), err.shape))

@@ -142,6 +142,21 @@ int bnmf_pass_time(bnmf_ctx* ctx, float* ms_avg, int* samples);
 int bnmf_pass_info(bnmf_ctx* ctx, int* out4);
 void* bnmf_stream(bnmf_ctx* ctx);
 
+/* One kernel of the reference's lower-level public API on the data (bnmf_set_dense: the
+ * already-shifted V + kappa, passed with kappa = 0) and the factor pair (bnmf_set_factors:
+ * (w, h), or the anchor (w~, h~) of the joint kernels) the context holds.  p carries beta,
+ * gamma, kappa (the shift of the model product), floor.
+ *   BNMF_OP_OBJECTIVE  out[0] = D_beta(V | W H + kappa)            core.objective, core.py:275-306
+ *   BNMF_OP_KKT        out[0..1] = res_W, res_H                   diagnostics.py:46-59
+ *   BNMF_OP_BMM_W      out = F x K  bmm_update_w(v, w, h)          updates.py:157-170
+ *   BNMF_OP_BMM_H      out = K x N  bmm_update_h(v, w, h)          updates.py:173-181
+ *   BNMF_OP_JMM_W      out = F x K  jmm_update_w(v, anchor, cur = h_current (K x N))   :203-220
+ *   BNMF_OP_JMM_H      out = K x N  jmm_update_h(v, anchor, cur = w_current (F x K))   :223-235
+ * cur and out are fp64 row-major host arrays (cur is NULL where unused). */
+enum { BNMF_OP_OBJECTIVE = 0, BNMF_OP_KKT = 1, BNMF_OP_BMM_W = 2, BNMF_OP_BMM_H = 3,
+       BNMF_OP_JMM_W = 4, BNMF_OP_JMM_H = 5 };
+int bnmf_kernel(bnmf_ctx* ctx, int op, const bnmf_params* p, const double* cur, double* out);
+
 #ifdef __cplusplus
 }
 #endif

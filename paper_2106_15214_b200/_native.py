@@ -80,7 +80,10 @@ _SIGS = {
     "bnmf_pass_time": ([C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_int)], C.c_int),
     "bnmf_pass_info": ([C.c_void_p, C.POINTER(C.c_int)], C.c_int),
     "bnmf_data_stats": ([C.c_void_p, C.POINTER(C.c_double)], C.c_int),
+    "bnmf_kernel": ([C.c_void_p, C.c_int, C.POINTER(Params), C.c_void_p, C.c_void_p], C.c_int),
 }
+
+OP_OBJECTIVE, OP_KKT, OP_BMM_W, OP_BMM_H, OP_JMM_W, OP_JMM_H = range(6)
 
 
 def load(path=LIB_PATH):
@@ -256,6 +259,29 @@ class Context:
         h = np.empty((self.K, self.N))
         self._check(self.lib.bnmf_get_factors(self.h, _ptr(w), _ptr(h)))
         return w, h
+
+    def kernel(self, op, params, cur=None):
+        """One kernel of the reference's lower-level API (include/bnmf.h: bnmf_kernel) on the
+        data and factor pair this context holds; returns a float (objective), a pair (KKT) or
+        the updated factor."""
+        if op in (OP_BMM_W, OP_JMM_W):
+            out = np.empty((self.F, self.K))
+        elif op in (OP_BMM_H, OP_JMM_H):
+            out = np.empty((self.K, self.N))
+        else:
+            out = np.empty(2)
+        if cur is not None:
+            cur = np.ascontiguousarray(cur, dtype=np.float64)
+            want = (self.K, self.N) if op == OP_JMM_W else (self.F, self.K)
+            if cur.shape != want:
+                raise ValueError(f"current factor has shape {cur.shape}, expected {want}")
+        self._check(self.lib.bnmf_kernel(self.h, int(op), C.byref(params),
+                                         _ptr(cur) if cur is not None else None, _ptr(out)))
+        if op == OP_OBJECTIVE:
+            return float(out[0])
+        if op == OP_KKT:
+            return float(out[0]), float(out[1])
+        return out
 
     def launches_per_iter(self):
         n = C.c_int(0)

@@ -791,6 +791,83 @@ struct Engine : EngineBase {
     return 0;
   }
 
+  // One update kernel / diagnostic of the reference's lower-level API (bnmf.h: bnmf_kernel)
+  // on the reference-order kernels: slot 0 of a one-iteration run state.
+  int kernel_op(int op, const bnmf_params* pp, const double* cur, double* out) override {
+    if (!V || !Wt) return fail(BNMF_E_STATE, "data and factors must be set first");
+    if (!out) return fail(BNMF_E_ARG, "null output");
+    bnmf_params q = *pp;
+    q.schedule = BNMF_SCHED_REFERENCE;
+    q.compute_kkt = op == BNMF_OP_KKT ? 1 : 0;
+    if (int rc = begin(&q, 1)) return rc;
+    const size_t fk = size_t(F) * K, nk = size_t(N) * K;
+    const int den_ones = (bc == BC_1) ? 1 : 0;
+    if (int rc = ensure_staging(std::max(fk, nk) * sizeof(double))) return rc;
+    double* stg = reinterpret_cast<double*>(staging);
+    if (op == BNMF_OP_JMM_W || op == BNMF_OP_JMM_H) {
+      if (!cur) return fail(BNMF_E_ARG, "the joint kernels need the current factor");
+      if (op == BNMF_OP_JMM_W) {   // h_current -> Hc (N x K)
+        if (int rc = h2d_bounce(stg, cur, nk * sizeof(double))) return rc;
+        transpose_in<T><<<grid_for(nk), 256, 0, stream>>>(stg, K, size_t(N), Hc);
+      } else {                     // w_current -> Wc
+        if (int rc = h2d_bounce(stg, cur, fk * sizeof(double))) return rc;
+        from_double<T><<<grid_for(fk), 256, 0, stream>>>(stg, fk, Wc);
+      }
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(stream));
+    }
+    int rc = 0;
+    bool w_out = false, h_out = false;
+    switch (op) {
+      case BNMF_OP_OBJECTIVE: {
+        if ((rc = objective(Wt, Ht, 0))) return rc;
+        sum_small<<<1, 1024, 0, stream>>>(opart, n_oblocks, comm + 2 * fk, st, 0);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out, comm + 2 * fk, sizeof(double), cudaMemcpyDeviceToHost, stream));
+        break;
+      }
+      case BNMF_OP_KKT: {
+        if ((rc = enqueue_kkt(0))) return rc;
+        CK(cudaMemcpyAsync(out, tr_kkt, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+        break;
+      }
+      case BNMF_OP_BMM_W:
+        if ((rc = w_update(Wt, Ht, Ht, Ht, Wt, Wc, 0))) return rc;
+        w_out = true;
+        break;
+      case BNMF_OP_BMM_H:
+        if (den_ones && (rc = colsums(Wt, 0))) return rc;
+        if ((rc = hside(PM_UPDATE, Wt, Ht, Wt, Wt, Ht, Hc, den_ones, 0))) return rc;
+        h_out = true;
+        break;
+      case BNMF_OP_JMM_W:
+        if ((rc = chi(Hc, Ht, C1h, C2h, nk, 0))) return rc;
+        if ((rc = w_update(Wt, Ht, C1h, C2h, Wt, Wc, 0))) return rc;
+        w_out = true;
+        break;
+      case BNMF_OP_JMM_H:
+        if ((rc = chi(Wc, Wt, C1w, C2w, fk, 0))) return rc;
+        if (den_ones && (rc = colsums(C2w, 0))) return rc;
+        if ((rc = hside(PM_UPDATE, Wt, Ht, C1w, C2w, Ht, Hc, den_ones, 0))) return rc;
+        h_out = true;
+        break;
+      default:
+        return fail(BNMF_E_ARG, "unknown kernel operation");
+    }
+    if (w_out) {
+      to_double<T><<<grid_for(fk), 256, 0, stream>>>(Wc, fk, stg);
+      CK(cudaGetLastError());
+      if ((rc = d2h_bounce(out, stg, fk * sizeof(double)))) return rc;
+    } else if (h_out) {
+      transpose_out<T><<<grid_for(nk), 256, 0, stream>>>(Hc, K, size_t(N), stg);
+      CK(cudaGetLastError());
+      if ((rc = d2h_bounce(out, stg, nk * sizeof(double)))) return rc;
+    }
+    CK(cudaStreamSynchronize(stream));
+    begun = false;
+    return 0;
+  }
+
   int init_comm(int r, int nr, const void* id, int64_t ng) override {
     CK(cudaSetDevice(device));
     rank = r; nranks = nr; n_global = ng;
@@ -871,6 +948,12 @@ int bnmf_set_dense(bnmf_ctx* ctx, const void* v, int src_dtype, int src_on_devic
   CTX_CHECK(ctx);
   if (!v) return set_err("null data", BNMF_E_ARG);
   return ctx->eng->set_dense(v, src_dtype, src_on_device, F, N, ld, kappa);
+}
+
+int bnmf_kernel(bnmf_ctx* ctx, int op, const bnmf_params* p, const double* cur, double* out) {
+  CTX_CHECK(ctx);
+  if (!p) return set_err("null params", BNMF_E_ARG);
+  return ctx->eng->kernel_op(op, p, cur, out);
 }
 
 int bnmf_data_stats(bnmf_ctx* ctx, double* out) {

@@ -42,6 +42,10 @@ struct EngineBase {
   virtual int read_trace(double* obj, double* sec, double* kkt, int64_t n) = 0;
   virtual int init_comm(int rank, int nranks, const void* id, int64_t n_global) = 0;
   virtual int set_profiling(int on) = 0;
+  virtual int kernel_op(int op, const bnmf_params* p, const double* cur, double* out) {
+    (void)op; (void)p; (void)cur; (void)out;
+    return fail(BNMF_E_UNSUPPORTED, "kernel operations need dense data");
+  }
   virtual int pass_time(float* ms_avg, int* samples) = 0;
   // [kind (0 none, 1 SIMT pair, 2 tcgen05), grid CTAs, cluster size, rows of cluster rank 0]
   // of the fused pass the last begin() selected

@@ -81,3 +81,27 @@ def test_sparse_layout_does_not_mutate_the_callers_matrix():
     assert np.array_equal(m.indices, before[0]) and np.array_equal(m.data, before[1])
     assert shape == (2, 3) and list(ix) == [0, 1, 2, 0, 1] and list(v) == [2, 3, 1, 5, 4]
     assert list(cp) == [0, 2, 4, 5] and list(v[pm]) == [2, 5, 3, 4, 1]
+
+
+def test_reference_public_names_are_exported():
+    """The solver-path names of the reference's __init__.py (betanmf/__init__.py:38-114)
+    resolve against the drop-in; the CPU-only audits of the bound (verify suites, aux_value,
+    finite-difference gradients, operation-count model) are out of scope."""
+    import paper_2106_15214_b200 as bn
+    names = ["Algorithm", "BenchReport", "BetaParam", "DataMatrix", "DivergenceDomainError",
+             "FactorPair", "FitResult", "KktResiduals", "MajorizerAnchor", "OpCounter",
+             "SolverConfig", "Termination", "UpdateKind", "beta_divergence", "bmm_update_h",
+             "bmm_update_w", "default_kappa", "fit", "format_report", "gamma_exponent",
+             "init_factors", "jmm_update_h", "jmm_update_w", "kkt_residuals", "load_matrix",
+             "match_columns", "normalize", "objective", "run_bench", "run_bmm", "run_jmm",
+             "save_factors", "save_trace", "should_stop", "summarize", "synthetic_low_rank"]
+    missing = [n for n in names if not hasattr(bn, n) or n not in bn.__all__]
+    assert not missing, missing
+    # the kernels are device-backed: without a device they raise, they never fall back
+    from paper_2106_15214_b200 import _native
+    if _native.device_count() == 0:
+        import numpy as np
+        import pytest
+        v = bn.synthetic_low_rank(6, 5, 2, noise=0.1, seed=1)
+        with pytest.raises(_native.NativeUnavailable):
+            bn.objective(v, bn.init_factors(6, 5, 2, seed=2), 1.0)

@@ -431,6 +431,125 @@ __global__ void __launch_bounds__(SP_THREADS) sp_pass_c(SpArgs a, const RunState
   }
 }
 
+
+// ---- KKT residuals of the finished iterate (diagnostics.py:46-59 at beta = 1) -----------
+// grad_core = 1 - V / (W~ H~) (all entries; 1 where V = 0), so
+//   grad_W = rowsum(H~) - (V / Vt) H~^T      rows:    the SDDMM of pass A on (W~_p, H~_p)
+//   grad_H = colsum(W~) - W~^T (V / Vt)      columns: pass B1/B2 in its joint form
+// Untimed like the reference's (the loop timer is moved past them).
+template <int KPL>
+__global__ void __launch_bounds__(SP_THREADS, 3) sp_kkt_a(SpArgs a, const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  __shared__ double red[SP_THREADS / 8];
+  __shared__ double s_den[SP_KMAX];
+  if ((threadIdx.x & 7) == 0) red[threadIdx.x >> 3] = 0.0;
+  for (int k = threadIdx.x; k < a.KL; k += blockDim.x) s_den[k] = k < a.K ? a.denw[k] : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane >> 3, sl = lane & 7, k0 = sl * KPL;
+  const int KL = a.KL;
+  for (int f = blockIdx.x * SP_WARPS + warp; f < a.F; f += gridDim.x * SP_WARPS) {
+    float w[KPL], num[KPL];
+    ld_row<KPL>(a.Wt + size_t(f) * KL + k0, w);
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) num[i] = 0.f;
+    const long long j0 = a.indptr[f], j1 = a.indptr[f + 1];
+    for (long long jj = j0; jj < j1; jj += 4 * SP_U) {
+      int n[SP_U];
+      float x[SP_U], h[SP_U][KPL];
+#pragma unroll
+      for (int u = 0; u < SP_U; ++u) {
+        const long long j = jj + 4 * u + grp;
+        n[u] = j < j1 ? a.indices[j] : 0;
+        x[u] = j < j1 ? a.vals[j] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < SP_U; ++u) ld_row<KPL>(a.Ht + size_t(n[u]) * KL + k0, h[u]);
+#pragma unroll
+      for (int u = 0; u < SP_U; ++u) {
+        const long long j = jj + 4 * u + grp;
+        const bool ok = j < j1;
+        float p = 0.f;
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) p = fmaf(w[i], h[u][i], p);
+        const float y = group_sum(p);
+        const float zz = ok ? x[u] / y : 0.f;
+        if (ok && sl == 0) a.z[j] = zz;
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) num[i] = fmaf(zz, h[u][i], num[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      num[i] += __shfl_xor_sync(0xffffffffu, num[i], 8);
+      num[i] += __shfl_xor_sync(0xffffffffu, num[i], 16);
+    }
+    {
+      // the row's 8 lanes of group 0 hold its KL entries; fixed shuffle tree, lane 0 adds
+      double t = 0.0;
+#pragma unroll
+      for (int i = 0; i < KPL; ++i)
+        if (k0 + i < a.K) t += fabs(fmin(double(w[i]), s_den[k0 + i] - double(num[i])));
+      t += __shfl_xor_sync(0xffffffffu, t, 1);
+      t += __shfl_xor_sync(0xffffffffu, t, 2);
+      t += __shfl_xor_sync(0xffffffffu, t, 4);
+      if (lane == 0) red[threadIdx.x >> 3] += t;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < SP_THREADS / 8; ++i) t += red[i];
+    a.pc[blockIdx.x] = t;
+  }
+}
+
+// sum_nk |min(H~[n,k], colsum(W~)[k] - num[n,k])| per block (same thread map as pass B3)
+__global__ void __launch_bounds__(SP_THREADS) sp_kkt_h(SpArgs a, const double* comm_a,
+                                                       const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  const int KL = a.KL, cpb = SP_THREADS / KL;
+  const int k = threadIdx.x % KL, c = threadIdx.x / KL;
+  __shared__ double red[SP_THREADS];
+  double rs = 0.0;
+  if (c < cpb && k < a.K) {
+    const double cs = comm_a[k] / a.norms[k];   // colsum(W_p) / ||W_p[:, k]|| = colsum(W~_p)
+    for (int n = blockIdx.x * cpb + c; n < a.N; n += gridDim.x * cpb) {
+      const size_t t = size_t(n) * KL + k;
+      rs += fabs(fmin(double(a.Ht[t]), cs - double(a.num[t])));
+    }
+  }
+  red[threadIdx.x] = rs;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < SP_THREADS; ++i) s += red[i];
+    a.pb[blockIdx.x] = s;
+  }
+}
+__global__ void sp_kkt_sum(const double* pc, int GC, const double* pb, int GB, double* out2,
+                           RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  double s = 0.0;
+  for (int g = 0; g < GC; ++g) s += pc[g];
+  out2[0] = s;
+  s = 0.0;
+  for (int g = 0; g < GB; ++g) s += pb[g];
+  out2[1] = s;
+}
+__global__ void sp_kkt_finish(const double* in2, double fk, double kn, double* tr_kkt,
+                              RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  const long long it = st->base + slot;
+  tr_kkt[2 * (it - 1) + 0] = in2[0] / fk;
+  tr_kkt[2 * (it - 1) + 1] = in2[1] / kn;
+  // the loop timer does not see the KKT passes (solver.py:312-314)
+  st->t_last += globaltimer() - st->t_begin;
+}
+__global__ void sp_kkt_begin(RunState* st, int slot) {
+  if (iter_active(st, slot)) st->t_begin = globaltimer();
+}
+
 // fixed-order reduction of the pass-A partials -> comm[0:2K] (colsum, sumsq)
 __global__ void sp_reduce_a(const double* pa, int G, int K, double* comm, const RunState* st,
                             int slot) {
@@ -909,6 +1028,39 @@ struct SparseEngine : EngineBase {
     }
   }
 
+  // KKT residuals of iterate base+slot: W~_p = Wt (pass C done), H~_p = Hn (before the swap),
+  // rowsum(H~_p) = denw (sp_finish done), colsum(W~_p) = comm[k] / norms[k]
+  int enqueue_kkt(const SpArgs& a, int slot) {
+    SpArgs k = a;
+    k.Ht = Hn;
+    k.algorithm = BNMF_JMM;   // pass B1 in its joint form: W~^T Z with the Z written below
+    sp_kkt_begin<<<1, 1, 0, stream>>>(st, slot);
+    const int kpl = KL / 8;
+    if (kpl == 4) sp_kkt_a<4><<<GA, SP_THREADS, 0, stream>>>(k, st, slot);
+    else if (kpl == 8) sp_kkt_a<8><<<GA, SP_THREADS, 0, stream>>>(k, st, slot);
+    else sp_kkt_a<16><<<GA, SP_THREADS, 0, stream>>>(k, st, slot);
+    dispatch(1, k, slot);
+    sp_pass_b2<<<nsm * 8, 256, 0, stream>>>(k, st, slot);
+    if (NH > 0) {
+      sp_pass_b2h<<<NH, 1024, 0, stream>>>(k, st, slot);
+      ++launches;
+    }
+    SCK(cudaGetLastError());
+    launches += 3;
+    if (int rc = allreduce(num, size_t(N) * KL, ncclFloat)) return rc;
+    sp_kkt_h<<<GB3, SP_THREADS, 0, stream>>>(k, comm, st, slot);
+    double* k2 = comm + 2 * K + 4;
+    sp_kkt_sum<<<1, 1, 0, stream>>>(pc, GA, pb, GB3, k2, st, slot);
+    SCK(cudaGetLastError());
+    launches += 2;
+    if (int rc = allreduce(k2, 1, ncclDouble)) return rc;   // rows (res_W) are sharded
+    const double fg = double(nranks > 1 ? n_global : F);
+    sp_kkt_finish<<<1, 1, 0, stream>>>(k2, fg * K, double(K) * N, tr_kkt, st, slot);
+    SCK(cudaGetLastError());
+    launches += 1;
+    return 0;
+  }
+
   int enqueue_iteration(int slot) {
     SpArgs a = args();
     double* cobj = comm + 2 * K;
@@ -941,6 +1093,9 @@ struct SparseEngine : EngineBase {
     sp_finish<<<1, 128, 0, stream>>>(pb, GB3, K, comm, norms, denw, cobj, st, slot);
     SCK(cudaGetLastError());
     launches += 3;
+    if (p.compute_kkt) {
+      if (int rc = enqueue_kkt(a, slot)) return rc;
+    }
     // H~_p becomes the next iterate
     std::swap(Ht, Hn);
     SCK(cudaGetLastError());

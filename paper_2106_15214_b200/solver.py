@@ -476,7 +476,7 @@ def csr_with_csc_view(data):
 
 
 def _run_sparse(data, config, counter, algorithm, *, dtype="fp32", init=None, device=None,
-                kkt=False, schedule="auto", sharded=False):
+                kkt=True, schedule="auto", sharded=False):
     """Sparse KL path (config 5): beta = 1, kappa = 0, fp32 on the device.
 
     The reference densifies sparse input (matrixio.py:115-128) and would apply
@@ -542,11 +542,11 @@ def _run_sparse(data, config, counter, algorithm, *, dtype="fp32", init=None, de
         if sharded:
             _attach_comm(ctx, f_global)
         ctx.set_factors(w_init, h_init)
-        params = make_params(config, 0.0, kkt=False, schedule="reference")
+        params = make_params(config, 0.0, kkt=kkt, schedule="reference")
         done, converged = ctx.run(params, config.max_outer_iters)
         obj, sec, kk = ctx.trace(done)
         w, h = ctx.factors()
-    trace = [TraceRow(i + 1, float(obj[i]), float(sec[i]), float("nan"), float("nan"))
+    trace = [TraceRow(i + 1, float(obj[i]), float(sec[i]), float(kk[i, 0]), float(kk[i, 1]))
              for i in range(done)]
     _count_ops(counter, config, done)
     try:

@@ -214,6 +214,7 @@ def configs(only_sparse=False):
         out[f"cfg5p_{algo}/w"] = w
         out[f"cfg5p_{algo}/h"] = h
         out[f"cfg5p_{algo}/obj"] = obj
+        out[f"cfg5p_{algo}/kkt"] = kkt
     out["cfg5p/nnz"] = np.array(idx.size)
     out["cfg5p/vsum"] = np.array(float(vals.astype(np.float64).sum()))
     np.savez_compressed(path, **out)

@@ -150,6 +150,14 @@ def test_sparse_kl_matches_dense_reference():
         obj = np.array([r.objective for r in res.trace])
         assert max_rel(obj, ref) <= 1e-4, (algo, max_rel(obj, ref))
         assert res.factors.w.shape == (2000, 16) and res.factors.h.shape == (16, 400)
+        # the trace carries the KKT residuals of every iterate like the reference's
+        # (diagnostics.py:46-59); fp32 gradients are differences of sums
+        kkt = np.array([[r.kkt_w, r.kkt_h] for r in res.trace])
+        np.testing.assert_allclose(kkt, z[f"cfg5p_{algo}/kkt"], rtol=2e-3)
+        # and they are outside the loop timer: kkt=False gives the same iterates
+        res2 = bn.fit(csr, cfg, init=(w0, h0), dtype="fp32", kkt=False)
+        assert [r.objective for r in res2.trace] == [r.objective for r in res.trace]
+        assert np.isnan(res2.trace[-1].kkt_w)
 
 
 def test_sparse_matches_oracle_restatement_and_is_deterministic():

@@ -37,6 +37,8 @@ CONFIGS = {
     2: dict(F=1024, N=8192, K=32, beta=2.0, dtype="fp32", kappa=0.0),
     3: dict(F=1025, N=16384, K=20, beta=0.0, dtype="fp32", kappa=None),
     4: dict(F=256, N=4194304, K=12, beta=1.5, dtype="fp32", kappa=0.0),
+    # sparse KL (CSR, 0.05 % density -> 10^8 nonzeros, Zipf(1.1) columns), row-sharded
+    5: dict(F=1000000, N=200000, K=64, beta=1.0, dtype="fp32", kappa=0.0, density=5e-4),
 }
 
 
@@ -263,10 +265,101 @@ def workload_config(args, world):
             else "input fits in L2 (no flush; iterations re-read V)"}
 
 
+def run_sparse(args):
+    """Config 5: the sparse KL path (CSR on the device, SDDMM at the nonzeros).
+
+    value = device-timed iterations/s (kkt=False, like the dense configs); the roofline is the
+    byte model of SURVEY.md §8(d): CSR index + value (8 B per nonzero), W~ read + W written,
+    H~ read + H numerators written, over the measured HBM bandwidth, for the whole iteration
+    (the path is several kernels; none dominates).  cpu_baseline = the scipy.sparse restatement
+    of the reference loop (oracle.run_sparse_kl; the reference itself densifies and cannot
+    ingest config 5) on a row prefix, scaled by rows."""
+    rank, world, local = dist_env()
+    if world > 1:
+        raise SystemExit("bench.py --config 5 measures one GPU (row sharding is covered by "
+                         "tests/test_parallel_gloo.py)")
+    import scipy.sparse as sp
+    import torch
+    torch.cuda.set_device(local)
+    import paper_2106_15214_b200 as bn
+    from paper_2106_15214_b200 import solver, synthetic as syn
+    c = CONFIGS[5]
+    t0 = time.perf_counter()
+    indptr, idx, vals, shape = syn.config5(F=c["F"], N=c["N"], density=c["density"])
+    F, N = shape
+    nnz = int(vals.size)
+    gen_s = time.perf_counter() - t0
+    w0, h0 = syn.uniform_init(F, N, c["K"], seed=100 + c["K"])
+    csr = sp.csr_matrix((vals, idx, indptr), shape=shape)
+    arrays, _ = solver.csr_with_csc_view(csr)
+    config = bn.SolverConfig(beta=1.0, rank=c["K"], algorithm=args.algo, tol=1e-300, kappa=0.0,
+                             max_outer_iters=args.warmup + args.steps + 1)
+    ctx = solver.get_context(local, "fp32-sparse")
+    ctx.set_csr(*arrays, (F, N))
+    ctx.set_factors(w0, h0)
+    ctx.begin(solver.make_params(config, 0.0, kkt=False, schedule="reference"),
+              args.warmup + args.steps + 1)
+    ctx.step(args.warmup)
+    ctx.sync()
+    clocks = ClockSampler(local)
+    with clocks:
+        ms = ctx.step_timed(args.steps)
+    ctx.step(1)   # the trailing slot finishes the last iterate's trace row
+    done, _ = ctx.sync()
+    if done < args.warmup + args.steps:
+        raise RuntimeError(f"only {done} iterations ran")
+    obj, _, _ = ctx.trace(done)
+    launches = ctx.launches_per_iter()
+    value = args.steps / (ms / 1e3)
+    hbm, _, peak_src = measured_peaks()
+    bytes_iter = 8 * nnz + 8 * (F + 1) + 2 * F * c["K"] * 4 + 2 * N * c["K"] * 4
+    achieved = bytes_iter / (ms / args.steps / 1e3) / 1e9
+    out = {
+        "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"config5: sparse KL {args.algo} {F}x{N} CSR nnz={nnz} K={c['K']} fp32",
+                   "F": F, "N": N, "K": c["K"], "beta": 1.0, "algorithm": args.algo, "nnz": nnz,
+                   "parallelism": "rows x1", "l2": "inputs larger than L2"},
+        "schedule": "sparse", "gpu_launches": launches * args.steps,
+        "roofline": {"bound": "hbm", "kernel": "sparse iteration (sp_pass_a + sp_pass_b* + sp_pass_c)",
+                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": None, "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
+                     "algorithmic_bytes_per_launch": bytes_iter,
+                     "bytes_model": "8 B per nonzero (CSR index + value) + indptr + W~ read + W "
+                                    "written + H~ read + H numerators written (SURVEY.md 8d)"},
+        "clocks": clocks.summary(), "final_objective": float(obj[done - 1]),
+        "iterations_done": int(done), "generation_s": round(gen_s, 1),
+    }
+    if not args.no_cpu:
+        from oracle import betanmf_oracle as O
+        from threadpoolctl import threadpool_limits
+        fs = 50000
+        sub = csr[:fs].astype(np.float64)
+        with threadpool_limits(limits=os.cpu_count() or 1):
+            t0 = time.perf_counter()
+            O.run_sparse_kl(sub, c["K"], args.algo, max_outer_iters=2, init=(w0[:fs], h0))
+            dt = (time.perf_counter() - t0) / 2
+        out["cpu_baseline"] = {
+            "value": 1.0 / (dt * F / fs), "unit": "iterations/s", "cores": os.cpu_count() or 1,
+            "kind": "port",
+            "sample": f"scipy.sparse restatement of the reference loop (oracle.run_sparse_kl; the "
+                      f"reference densifies and cannot ingest config 5); first {fs} of {F} rows "
+                      f"({sub.nnz} nonzeros), 2 iterations, {dt * 1e3:.0f} ms each; value = 1 / "
+                      f"(that x {F // fs})"}
+    print(json.dumps(out))
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.impl == "reference" and args.config != 5:
         run_reference(args)
+        return
+    if args.config == 5:
+        if args.impl == "reference":
+            raise SystemExit("the reference arm of config 5 is the cpu_baseline of the default arm")
+        run_sparse(args)
         return
     rank, world, local = dist_env()
     import torch

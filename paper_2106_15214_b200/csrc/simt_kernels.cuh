@@ -7,11 +7,25 @@
 // V is F x ldv row-major; W is F x K row-major; H is stored transposed
 // ("Ht", N x K row-major, k contiguous per column n).  All reductions are
 // fixed-order (no float atomics): results are bitwise reproducible.
+//
+// fp64 (T = double) forms every product on the FP64 tensor path: the 32 x 32 model tile
+// W H^T and the skinny side products are chains of mma.sync.m8n8k4.f64 (SASS: DMMA) on
+// 8 x 8 sub-tiles, accumulators in the D fragments; fp32 keeps the scalar FMA form.
 #pragma once
+
+#include <type_traits>
 
 #include "bnmf_common.cuh"
 
 namespace bnmf {
+
+// D (8 x 8) += A (8 x 4, row) * B (4 x 8, col) in fp64.  Fragments of lane L (g = L / 4,
+// t = L % 4): a = A[g][t], b = B[t][g], d[0..1] = D[g][2 t + {0, 1}].
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
 
 constexpr int ST_TF = 32;       // rows of F per tile
 constexpr int ST_NC = 32;       // columns of N per tile
@@ -41,6 +55,41 @@ template <int BC, int MODE, typename T>
 __device__ __forceinline__ void z_tile(const T* __restrict__ V, size_t ldv, int F, int N,
                                        int f0, int n0, const T* Ws, const T* Hs, int K,
                                        int ks, T kappa, T beta, T* Zn, T* Zd) {
+  if constexpr (std::is_same<T, double>::value) {
+    // warp w: f sub-tile r = w & 3, n sub-tiles 2 (w >> 2) + {0, 1}; lane (g, t) ends up with
+    // y at rows 8 r + g, columns 8 c + 2 t + {0, 1}
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = w & 3, cp = w >> 2, g = lane >> 2, t = lane & 3;
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      const int k = k0 + t;
+      const double a = k < K ? Ws[(8 * r + g) * ks + k] : 0.0;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const double b = k < K ? Hs[(8 * (2 * cp + c) + g) * ks + k] : 0.0;
+        dmma884(acc[c], a, b);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int f = 8 * r + g, n = 8 * (2 * cp + c) + 2 * t + e;
+        T zn = T(0), zd = T(0);
+        if (f0 + f < F && n0 + n < N) {
+          const T y = acc[c][e] + kappa;
+          const T x = V[(size_t)(f0 + f) * ldv + (n0 + n)];
+          if (MODE == PM_KKT) {
+            zn = grad_core<BC, T>(x, y, beta);
+          } else {
+            bases<BC, T>(x, y, beta, zn, zd);
+          }
+        }
+        Zn[f * (ST_NC + 1) + n] = zn;
+        Zd[f * (ST_NC + 1) + n] = zd;
+      }
+    return;
+  }
   for (int e = threadIdx.x; e < ST_TF * ST_NC; e += blockDim.x) {
     int f = e / ST_NC, n = e - f * ST_NC;
     T zn = T(0), zd = T(0);
@@ -90,6 +139,57 @@ wside_partials(const T* __restrict__ V, size_t ldv, int F, int N, int K,
   const T kappa = T(sc.kappa), beta = T(sc.beta);
 
   load_rows(Ws, Wp + (size_t)f0 * K, ST_TF, F - f0, K, ks);
+
+  if constexpr (std::is_same<T, double>::value) {
+    // DMMA accumulation: warp w owns rows 8 r + [0, 8) (r = w & 3) and the k sub-tiles
+    // kc = (w >> 2) + 2 j; the sums over the whole segment stay in the D fragments
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = w & 3, kp = w >> 2, g = lane >> 2, t = lane & 3;
+    constexpr int NJ = ST_KMAX / 16;
+    double dn[NJ][2], dd[NJ][2];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) { dn[j][0] = dn[j][1] = 0.0; dd[j][0] = dd[j][1] = 0.0; }
+    for (int n0 = nbeg; n0 < nend; n0 += ST_NC) {
+      __syncthreads();
+      int valid = min(ST_NC, nend - n0);
+      load_rows(Hs, Hp + (size_t)n0 * K, ST_NC, valid, K, ks);
+      load_rows(C1s, C1 + (size_t)n0 * K, ST_NC, valid, K, ks);
+      if (MODE != PM_KKT) load_rows(C2s, C2 + (size_t)n0 * K, ST_NC, valid, K, ks);
+      __syncthreads();
+      z_tile<BC, MODE, T>(V, ldv, F, nend, f0, n0, Ws, Hs, K, ks, kappa, beta, Zn, Zd);
+      __syncthreads();
+#pragma unroll 2
+      for (int n4 = 0; n4 < ST_NC / 4; ++n4) {
+        const double an = Zn[(8 * r + g) * (ST_NC + 1) + 4 * n4 + t];
+        const double ad = Zd[(8 * r + g) * (ST_NC + 1) + 4 * n4 + t];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const int kk = 8 * (kp + 2 * j) + g;
+          if (8 * (kp + 2 * j) < K) {
+            const double b1 = kk < K ? C1s[(4 * n4 + t) * ks + kk] : 0.0;
+            dmma884(dn[j], an, b1);
+            if (MODE != PM_KKT) {
+              const double b2 = kk < K ? C2s[(4 * n4 + t) * ks + kk] : 0.0;
+              dmma884(dd[j], ad, b2);
+            }
+          }
+        }
+      }
+    }
+    const int f = f0 + 8 * r + g;
+    if (f < F) {
+      double* pn = part + ((size_t)seg * 2 + 0) * F * K + (size_t)f * K;
+      double* pd = part + ((size_t)seg * 2 + 1) * F * K + (size_t)f * K;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int k = 8 * (kp + 2 * j) + 2 * t + e;
+          if (k < K) { pn[k] = dn[j][e]; pd[k] = dd[j][e]; }
+        }
+    }
+    return;
+  }
 
   const int fl = threadIdx.x & 31;   // row within the tile
   const int kg = threadIdx.x >> 5;   // k group (warp-uniform)
@@ -164,6 +264,80 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
   const int valid_n = min(ST_NC, N - n0);
   const T kappa = T(sc.kappa), beta = T(sc.beta);
   load_rows(Hs, Hp + (size_t)n0 * K, ST_NC, valid_n, K, ks);
+
+  if constexpr (std::is_same<T, double>::value) {
+    // DMMA accumulation: D rows = k (sub-tiles kc = (w >> 2) + 2 j), D columns = n
+    // (sub-tile c = w & 3); lane (g, t) ends up with (k = 8 kc + g, n = 8 c + 2 t + {0, 1})
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = w & 3, kp = w >> 2, g = lane >> 2, t = lane & 3;
+    constexpr int NJ = ST_KMAX / 16;
+    double dn[NJ][2], dd[NJ][2];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) { dn[j][0] = dn[j][1] = 0.0; dd[j][0] = dd[j][1] = 0.0; }
+    const bool use_den = (MODE != PM_KKT) && !den_ones;
+    for (int f0 = 0; f0 < F; f0 += ST_TF) {
+      __syncthreads();
+      int valid_f = min(ST_TF, F - f0);
+      load_rows(Ws, Wp + (size_t)f0 * K, ST_TF, valid_f, K, ks);
+      if (MODE != PM_KKT) {
+        load_rows(C1s, C1w + (size_t)f0 * K, ST_TF, valid_f, K, ks);
+        if (use_den) load_rows(C2s, C2w + (size_t)f0 * K, ST_TF, valid_f, K, ks);
+      }
+      __syncthreads();
+      z_tile<BC, MODE, T>(V, ldv, F, N, f0, n0, Ws, Hs, K, ks, kappa, beta, Zn, Zd);
+      __syncthreads();
+      const T* A1 = (MODE == PM_KKT) ? Ws : C1s;
+#pragma unroll 2
+      for (int f4 = 0; f4 < ST_TF / 4; ++f4) {
+        const double bn = Zn[(4 * f4 + t) * (ST_NC + 1) + 8 * c + g];
+        const double bd = Zd[(4 * f4 + t) * (ST_NC + 1) + 8 * c + g];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const int kk = 8 * (kp + 2 * j) + g;
+          if (8 * (kp + 2 * j) < K) {
+            const double a1 = kk < K ? A1[(4 * f4 + t) * ks + kk] : 0.0;
+            dmma884(dn[j], a1, bn);
+            if (use_den) {
+              const double a2 = kk < K ? C2s[(4 * f4 + t) * ks + kk] : 0.0;
+              dmma884(dd[j], a2, bd);
+            }
+          }
+        }
+      }
+    }
+    if (MODE == PM_KKT) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int k = 8 * (kp + 2 * j) + g, n = 8 * c + 2 * t + e;
+          if (k < K && n < valid_n) s += fabs(fmin(double(Hs[n * ks + k]), dn[j][e]));
+        }
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+      if (lane == 0) red[w] = s;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double tt = 0.0;
+        for (int ww = 0; ww < ST_THREADS / 32; ++ww) tt += red[ww];
+        part[blockIdx.x] = tt;
+      }
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int k = 8 * (kp + 2 * j) + g, n = 8 * c + 2 * t + e;
+        if (k < K && n < valid_n) {
+          const double den = den_ones ? colsum_c2[k] : dd[j][e];
+          const double rr = dn[j][e] / fmax(den, sc.floor);
+          const double b = double(Hbase[(size_t)(n0 + n) * K + k]);
+          Hout[(size_t)(n0 + n) * K + k] = T(b * apply_exponent<double>(rr, sc.gamma));
+        }
+      }
+    return;
+  }
 
   const int nl = threadIdx.x & 31;
   const int kg = threadIdx.x >> 5;
@@ -259,6 +433,31 @@ objective_partials(const T* __restrict__ V, size_t ldv, int F, int N, int K,
     __syncthreads();
     load_rows(Hs, Ht + (size_t)n0 * K, ST_NC, min(ST_NC, nend - n0), K, ks);
     __syncthreads();
+    if constexpr (std::is_same<T, double>::value) {
+      const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      const int r = w & 3, cp = w >> 2, g = lane >> 2, t = lane & 3;
+      double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      for (int k0 = 0; k0 < K; k0 += 4) {
+        const int k = k0 + t;
+        const double a = k < K ? Ws[(8 * r + g) * ks + k] : 0.0;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const double b = k < K ? Hs[(8 * (2 * cp + c) + g) * ks + k] : 0.0;
+          dmma884(acc[c], a, b);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int f = 8 * r + g, n = 8 * (2 * cp + c) + 2 * t + e;
+          if (f0 + f < F && n0 + n < nend) {
+            const double x = double(V[(size_t)(f0 + f) * ldv + n0 + n]);
+            s += divergence<BC>(x, acc[c][e] + double(kappa), sc.beta);
+          }
+        }
+      continue;
+    }
     for (int e = threadIdx.x; e < ST_TF * ST_NC; e += blockDim.x) {
       int f = e / ST_NC, n = e - f * ST_NC;
       if (f0 + f < F && n0 + n < nend) {

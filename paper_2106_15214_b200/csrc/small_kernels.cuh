@@ -67,16 +67,24 @@ __global__ void update_w(const T* __restrict__ base, const double* __restrict__ 
   }
 }
 
-// Column sums of an F x K matrix (K threads, fixed order) -> double K-vector.
+// Column sums of an F x K matrix -> double K-vector.  One block of 256 threads per column:
+// thread t sums rows t, t + 256, ... in order, then a fixed shared-memory tree (deterministic).
 template <typename T>
-__global__ void col_sums(const T* __restrict__ M, int F, int K, double* __restrict__ out,
-                         const RunState* st, int slot) {
+__global__ void __launch_bounds__(256) col_sums(const T* __restrict__ M, int F, int K,
+                                                double* __restrict__ out, const RunState* st,
+                                                int slot) {
   if (st && !iter_active(st, slot)) return;
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= K) return;
+  const int k = blockIdx.x;
+  __shared__ double red[256];
   double s = 0.0;
-  for (int f = 0; f < F; ++f) s += double(M[(size_t)f * K + k]);
-  out[k] = s;
+  for (int f = threadIdx.x; f < F; f += 256) s += double(M[(size_t)f * K + k]);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[k] = red[0];
 }
 
 // norms[k] = sqrt(sum_f W[f,k]^2); Wn = W / norms (solver.py:167-171).

@@ -530,7 +530,7 @@ struct Engine : EngineBase {
   }
 
   int colsums(const T* M, int slot) {
-    col_sums<T><<<K, 256, 0, stream>>>(M, F, K, colsum, st, slot);
+    col_sums<T><<<(K + 31) / 32, 32, 0, stream>>>(M, F, K, colsum, st, slot);
     CK(cudaGetLastError());
     launches += 1;
     return 0;

@@ -24,6 +24,7 @@
 #include "fused_simt2.cuh"
 #include "fused_tc_kernel.cuh"
 #include "fused_tc2_kernel.cuh"
+#include "fused_tc3_kernel.cuh"
 #include "small_kernels.cuh"
 
 namespace bnmf {
@@ -52,6 +53,11 @@ struct FusedState {
   long long* prof = nullptr;   // BNMF_TC_PROF=1: wait-cycle counters [grid][48]
   int cap = 0;                 // BNMF_TC_MAX_CLUSTERS at creation (test knob)
   bool v1 = true;              // false with BNMF_TC_V2=1 (second-generation kernel, A/B knob)
+  // tcgen05 pass pair over a (column group, 128-row slice) grid: F > 256 or 16 < K <= 32
+  bool tc3 = false;
+  int t3_gx = 0, t3_r = 0, t3_kp = 16;
+  float* hpart = nullptr;      // [slice][N][num KP | den KP] H-side partial sums
+  double* kcomm = nullptr;     // KKT pass of the pair: grad_W (F x K) summed over the slabs
   double* kpart = nullptr;     // KKT pass: per-CTA sums of |min(H~, grad_H)|
   int kparts = 0;
   double* kcs = nullptr;       // KKT pass, beta = 1 on the SIMT pair: colsum(W~_p) (K)
@@ -63,6 +69,13 @@ struct FusedState {
 static bool env_tc_v1() {
   const char* c = getenv("BNMF_TC_V2");
   return !(c && c[0] == '1');
+}
+
+// BNMF_TC3=0 keeps the F > 256 / 16 < K <= 32 shapes on the SIMT pair (A/B knob)
+static bool tc3_wanted(int K) {
+  const char* e = getenv("BNMF_TC3");
+  const char* f = getenv("BNMF_FUSED_SIMT");
+  return K <= 32 && !(e && e[0] == '0') && !(f && f[0] == '1');
 }
 
 static int env_cluster_cap() {
@@ -223,8 +236,18 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
     if (fs->cap > 0) clusters = std::min(clusters, fs->cap);
     fs->tc_grid = fs->tc_cl * std::max(1, std::min(nb, clusters));
   }
-  int gmax = std::max(fs->tc_grid, fs->s2_S);
-  const int gobj = std::max(gmax, fs->s2_S * fs->s2_rc);
+  // BNMF_TC3=0 keeps these shapes on the SIMT pair (A/B knob)
+  fs->tc3 = !fs->tc && tc3_wanted(io.K) && encode_fn() != nullptr;
+  if (fs->tc3) {
+    const int nb = (io.N + ftc::BN - 1) / ftc::BN;
+    fs->t3_kp = io.K <= 16 ? 16 : 32;
+    fs->t3_r = (io.F + ftc::FR - 1) / ftc::FR;
+    fs->t3_gx = std::max(1, std::min(nb, nsm / fs->t3_r));
+    FCK(cudaMalloc(&fs->hpart, size_t(fs->t3_r) * io.N * 2 * fs->t3_kp * sizeof(float)));
+    FCK(cudaMalloc(&fs->kcomm, (size_t(2) * io.F * io.K + 8) * sizeof(double)));
+  }
+  int gmax = std::max(std::max(fs->tc_grid, fs->s2_S), fs->t3_gx);
+  const int gobj = std::max(std::max(gmax, fs->s2_S * fs->s2_rc), fs->t3_gx * fs->t3_r);
   const char* prof_env = getenv("BNMF_TC_PROF");
   if (fs->tc && prof_env && prof_env[0] == '1') {
     const size_t np = size_t(fs->tc_grid) * 288 + 3 * 4096;
@@ -237,7 +260,7 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
   FCK(cudaMalloc(&fs->kcs, io.K * sizeof(double)));
   FCK(cudaMalloc(&fs->part, size_t(gmax) * 2 * fk * sizeof(double)));
   FCK(cudaMalloc(&fs->opart, size_t(gobj) * sizeof(double)));
-  if (fs->tc) {
+  if (fs->tc || fs->tc3) {
     // V stages: [32 rows x 132 columns] boxes, unswizzled; the 4 extra
     // columns pad the SMEM rows to 528 B (conflict-free in both phases)
     cuuint64_t dims[2] = {cuuint64_t(io.N), cuuint64_t(io.F)};
@@ -257,9 +280,9 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
 
 void fused_destroy(FusedState* fs) {
   if (!fs) return;
-  float* fp[] = {fs->H[0], fs->H[1], fs->W2[0], fs->W2[1], fs->Wn, fs->C1, fs->C2};
+  float* fp[] = {fs->H[0], fs->H[1], fs->W2[0], fs->W2[1], fs->Wn, fs->C1, fs->C2, fs->hpart};
   for (float* q : fp) if (q) cudaFree(q);
-  double* dp[] = {fs->norms, fs->csum2, fs->part, fs->opart, fs->kpart, fs->kcs};
+  double* dp[] = {fs->norms, fs->csum2, fs->part, fs->opart, fs->kpart, fs->kcs, fs->kcomm};
   for (double* q : dp) if (q) cudaFree(q);
   if (fs->prof) cudaFree(fs->prof);
   if (g_last_tc == fs) g_last_tc = nullptr;
@@ -332,8 +355,42 @@ static cudaError_t launch_tc_k(FusedState* fs, const FusedArgs& a, const FusedIO
   return launch_tc<FBC, false>(fs, a, io, slot, p_override);
 }
 
+template <int FBC, int KP>
+static cudaError_t launch_tc3(FusedState* fs, const FusedArgs& a, const FusedIO& io, int slot,
+                              int p_override) {
+  const dim3 grid(fs->t3_gx, fs->t3_r);
+  const int sm = int(ftc3::Lay<KP>::SMEM);
+  if (a.do_h && !a.kkt) {
+    auto hk = ftc3::pass_tc3<FBC, true, KP, ftc3::MODE_H>;
+    cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    hk<<<grid, ftc3::NTHREADS3, sm, io.stream>>>(a, fs->mapV, fs->hpart, io.st, slot, p_override);
+    const size_t nk = size_t(io.N) * io.K;
+    ftc3::tc3_h_finish<KP><<<int(std::min<size_t>((nk + 255) / 256, 148 * 8)), 256, 0, io.stream>>>(
+        a, fs->hpart, fs->t3_r, io.st, slot, p_override);
+  }
+  auto wk = ftc3::pass_tc3<FBC, true, KP, ftc3::MODE_W>;
+  cudaFuncSetAttribute(wk, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  wk<<<grid, ftc3::NTHREADS3, sm, io.stream>>>(a, fs->mapV, fs->hpart, io.st, slot, p_override);
+  return cudaGetLastError();
+}
+
+template <int FBC>
+static cudaError_t launch_tc3_k(FusedState* fs, const FusedArgs& a, const FusedIO& io, int slot,
+                                int p_override) {
+  if (fs->t3_kp == 16) return launch_tc3<FBC, 16>(fs, a, io, slot, p_override);
+  return launch_tc3<FBC, 32>(fs, a, io, slot, p_override);
+}
+
 static cudaError_t launch_pass(FusedState* fs, const FusedArgs& a, const FusedIO& io, int slot,
                                int p_override) {
+  if (fs->tc3 && a.kkt != 1) {   // kkt == 2: the W-side KKT pass of the pair
+    const double beta = io.sc.beta;
+    if (beta == 1.5) return launch_tc3_k<ftc::FBC_15>(fs, a, io, slot, p_override);
+    if (beta == 0.0) return launch_tc3_k<ftc::FBC_0>(fs, a, io, slot, p_override);
+    if (beta == 1.0) return launch_tc3_k<ftc::FBC_1>(fs, a, io, slot, p_override);
+    if (beta == 2.0) return launch_tc3_k<ftc::FBC_2>(fs, a, io, slot, p_override);
+    return launch_tc3_k<ftc::FBC_GEN>(fs, a, io, slot, p_override);
+  }
   if (fs->tc) {
     const double beta = io.sc.beta;
     if (beta == 1.5) return launch_tc_k<ftc::FBC_15>(fs, a, io, slot, p_override);
@@ -358,14 +415,14 @@ static int enqueue_pass_and_update(FusedState* fs, const FusedIO& io, int slot, 
   if (io.ev_a) FCK(record_event(io.ev_a, io.stream));
   FCK(launch_pass(fs, a, io, slot, p_override));
   if (io.ev_b) FCK(record_event(io.ev_b, io.stream));
-  const bool s2 = !fs->tc;
-  const int gpart = fs->tc ? fs->tc_grid : fs->s2_S;
-  const int gobj = s2 ? fs->s2_S * fs->s2_rc : gpart;
+  const bool s2 = !fs->tc && !fs->tc3;
+  const int gpart = fs->tc ? fs->tc_grid : (fs->tc3 ? fs->t3_gx : fs->s2_S);
+  const int gobj = fs->tc3 ? fs->t3_gx * fs->t3_r : (s2 ? fs->s2_S * fs->s2_rc : gpart);
   fused_reduce<<<int((fk2 + 1 + 255) / 256), 256, 0, io.stream>>>(
       fs->part, fs->opart, gpart, gobj, int(fk2), io.K,
       fs->tc ? fs->tc_f0 : io.F, fs->tc ? fs->tc_cl : 1, io.comm, io.st, slot, p_override);
   FCK(cudaGetLastError());
-  if (io.launches) *io.launches += (s2 && a.do_h) ? 3 : 2;
+  if (io.launches) *io.launches += fs->tc3 ? (a.do_h ? 4 : 2) : ((s2 && a.do_h) ? 3 : 2);
   if (io.nranks > 1) {
     ncclResult_t r = ncclAllReduce(io.comm, io.comm, fk2 + 1, ncclDouble, ncclSum, io.nccl,
                                    io.stream);
@@ -452,6 +509,30 @@ static __global__ void __launch_bounds__(1024) kkt_finish(const double* __restri
   }
 }
 
+// res_W from an explicit gradient (the pass pair's W-side KKT pass): grad[i] = kcomm[i]
+static __global__ void __launch_bounds__(1024) kkt_finish_g(const double* __restrict__ grad,
+                                                            const double* __restrict__ resh, WPair Wt2,
+                                                            int F, int K, double kn,
+                                                            double* __restrict__ tr_kkt,
+                                                            const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  const float* W = Wt2.w[iter_parity(st, slot, -1)];
+  const size_t fk = size_t(F) * K;
+  __shared__ double red[32];
+  double s = 0.0;
+  for (size_t i = threadIdx.x; i < fk; i += blockDim.x) s += fabs(fmin(double(W[i]), grad[i]));
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 32; ++w) t += red[w];
+    const long long it = st->base + slot;
+    tr_kkt[2 * (it - 1) + 0] = t / double(fk);
+    tr_kkt[2 * (it - 1) + 1] = *resh / kn;
+  }
+}
+
 static int enqueue_kkt(FusedState* fs, const FusedIO& io, int slot, std::string& err) {
   FusedArgs a = make_args(fs, io, 1);
   a.kkt = 1;
@@ -461,7 +542,7 @@ static int enqueue_kkt(FusedState* fs, const FusedIO& io, int slot, std::string&
   wp.w[0] = fs->W2[0]; wp.w[1] = fs->W2[1];
   const size_t fk2 = size_t(2) * io.F * io.K;
   int nparts = fs->tc_grid;
-  if (!fs->tc) {
+  if (!fs->tc) {   // SIMT pair and the tcgen05 pass pair: fs2::hpass in KKT mode
     nparts = (io.N + fs2::NC - 1) / fs2::NC;
     if (a.den_ones) {
       kkt_colsum<<<io.K, 256, 0, io.stream>>>(wp, io.F, io.K, fs->kcs, io.st, slot);
@@ -479,21 +560,43 @@ static int enqueue_kkt(FusedState* fs, const FusedIO& io, int slot, std::string&
     if (r != ncclSuccess) { err = std::string("ncclAllReduce: ") + ncclGetErrorString(r); return -1; }
     if (io.launches) *io.launches += 1;
   }
-  kkt_finish<<<1, 1024, 0, io.stream>>>(io.comm, wp, io.F, io.K,
-                                        double(io.K) * double(io.nranks > 1 ? io.n_global : io.N),
-                                        io.tr_kkt, io.st, slot);
+  const double kn = double(io.K) * double(io.nranks > 1 ? io.n_global : io.N);
+  if (fs->tc3) {
+    // the pair accumulates Num_W and Den_W in fp32 TMEM folds; their difference is not a
+    // usable gradient once they agree to a few digits, so grad_W gets its own W-side pass with
+    // the gradient core formed per element (FusedArgs::kkt == 2)
+    FusedArgs g = make_args(fs, io, 1);
+    g.kkt = 2;
+    FCK(launch_pass(fs, g, io, slot, -1));
+    fused_reduce<<<int((fk2 + 1 + 255) / 256), 256, 0, io.stream>>>(
+        fs->part, fs->opart, fs->t3_gx, fs->t3_gx * fs->t3_r, int(fk2), io.K, io.F, 1, fs->kcomm,
+        io.st, slot, -1);
+    FCK(cudaGetLastError());
+    if (io.launches) *io.launches += 2;
+    if (io.nranks > 1) {
+      ncclResult_t r = ncclAllReduce(fs->kcomm, fs->kcomm, fk2 / 2, ncclDouble, ncclSum, io.nccl,
+                                     io.stream);
+      if (r != ncclSuccess) { err = std::string("ncclAllReduce: ") + ncclGetErrorString(r); return -1; }
+      if (io.launches) *io.launches += 1;
+    }
+    kkt_finish_g<<<1, 1024, 0, io.stream>>>(fs->kcomm, io.comm + fk2 + 1, wp, io.F, io.K, kn,
+                                            io.tr_kkt, io.st, slot);
+  } else {
+    kkt_finish<<<1, 1024, 0, io.stream>>>(io.comm, wp, io.F, io.K, kn, io.tr_kkt, io.st, slot);
+  }
   FCK(cudaGetLastError());
   if (io.launches) *io.launches += 1;
   return 0;
 }
 
 bool fused_shape_matches(const FusedState* fs, int F, int N, int K) {
-  return fs && fs->F == F && fs->N == N && fs->K == K && (!fs->tc || (fs->cap == env_cluster_cap() && fs->v1 == env_tc_v1()));
+  return fs && fs->F == F && fs->N == N && fs->K == K && (!fs->tc || (fs->cap == env_cluster_cap() && fs->v1 == env_tc_v1())) &&
+         (fs->tc || fs->tc3 == tc3_wanted(K));
 }
 
 void fused_info(const FusedState* fs, int* out4) {
-  out4[0] = fs ? (fs->tc ? 2 : 1) : 0;
-  out4[1] = fs ? (fs->tc ? fs->tc_grid : fs->s2_S * fs->s2_rc) : 0;
+  out4[0] = fs ? ((fs->tc || fs->tc3) ? 2 : 1) : 0;
+  out4[1] = fs ? (fs->tc ? fs->tc_grid : (fs->tc3 ? fs->t3_gx * fs->t3_r : fs->s2_S * fs->s2_rc)) : 0;
   out4[2] = fs ? (fs->tc ? fs->tc_cl : 1) : 0;
   out4[3] = fs ? (fs->tc ? fs->tc_f0 : fs->F) : 0;
 }

@@ -449,20 +449,17 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
             float o0 = 0.f, o1 = 0.f;
 #pragma unroll
             for (int i = 0; i < 8; i += 2) {
-              zpair<FBC>(xx[i], yy[i], beta, zn[i], zd[i]);
-              zpair<FBC>(xx[i + 1], yy[i + 1], beta, zn[i + 1], zd[i + 1]);
-              dacc<FBC>(xx[i], yy[i], zd[i], beta, o0);
-              dacc<FBC>(xx[i + 1], yy[i + 1], zd[i + 1], beta, o1);
+              z_and_obj<FBC>(xx[i], yy[i], 0.f, beta, zn[i], zd[i], o0);
+              z_and_obj<FBC>(xx[i + 1], yy[i + 1], 0.f, beta, zn[i + 1], zd[i + 1], o1);
             }
             objb += o0 + o1;
           } else {
             float o0 = 0.f;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              zpair<FBC>(xx[i], yy[i], beta, zn[i], zd[i]);
               const bool ok = fok && (n0 + 32 * idx + c0 + 8 * s4 + i < N);
               float t = 0.f;
-              dacc<FBC>(xx[i], yy[i], zd[i], beta, t);
+              z_and_obj<FBC>(xx[i], yy[i], 0.f, beta, zn[i], zd[i], t);
               zn[i] = ok ? zn[i] : 0.f;
               zd[i] = ok ? zd[i] : 0.f;
               o0 += ok ? t : 0.f;

@@ -139,6 +139,79 @@ __device__ __forceinline__ void dacc(float x, float y, float zd, float beta, flo
   }
 }
 
+// Z and the objective term of one element from ONE reciprocal (W items of the item-team
+// kernels).  beta = 0 and beta = 1 need u = (x - y) / y for their cancellation-free objective
+// forms; divergence32 gets it from an IEEE division and a 14-term series, which made the W items
+// of these classes ~10x the H items.  Here u = (x - y) rcp(y) with the reciprocal Z needs anyway,
+// an 8-term Horner series for |u| < 1/8 (truncation < 2^-24 of the term) and the MUFU log beyond.
+template <int FBC>
+__device__ __forceinline__ void z_and_obj(float x, float y, float zd_in, float beta, float& zn,
+                                          float& zd, float& acc) {
+  (void)zd_in;
+  if (FBC == FBC_0) {
+    const float r = rcp_fast(y);
+    zd = r;
+    zn = x * r * r;
+    const float u = (x - y) * r;
+    float d;
+    if (fabsf(u) < 0.125f) {
+      // u - log1p(u) = u^2 (1/2 - u/3 + u^2/4 - ...)
+      float p = -0.1111111111f;
+      p = fmaf(p, u, 0.125f);
+      p = fmaf(p, u, -0.1428571429f);
+      p = fmaf(p, u, 0.1666666667f);
+      p = fmaf(p, u, -0.2f);
+      p = fmaf(p, u, 0.25f);
+      p = fmaf(p, u, -0.3333333333f);
+      p = fmaf(p, u, 0.5f);
+      d = p * u * u;
+    } else {
+      const float t = x * r;
+      d = t - __logf(t) - 1.f;
+    }
+    acc += d;
+  } else if (FBC == FBC_1) {
+    const float r = rcp_fast(y);
+    zn = x * r;
+    zd = 1.f;
+    const float u = (x - y) * r;
+    float d;
+    if (fabsf(u) < 0.125f) {
+      // (1 + u) log1p(u) - u = u^2 (1/2 - u/6 + u^2/12 - u^3/20 + ...), coefficient 1 / (j (j - 1))
+      float p = 0.0138888889f;            // 1 / 72
+      p = fmaf(p, u, -0.0178571429f);     // 1 / 56
+      p = fmaf(p, u, 0.0238095238f);      // 1 / 42
+      p = fmaf(p, u, -0.0333333333f);     // 1 / 30
+      p = fmaf(p, u, 0.05f);              // 1 / 20
+      p = fmaf(p, u, -0.0833333333f);     // 1 / 12
+      p = fmaf(p, u, 0.1666666667f);      // 1 / 6
+      p = fmaf(p, u, -0.5f);
+      d = -p * u * u * y;
+    } else if (x == 0.f) {
+      d = y;
+    } else {
+      d = x * __logf(x * r) - x + y;
+    }
+    acc += d;
+  } else {
+    zpair<FBC>(x, y, beta, zn, zd);
+    dacc<FBC>(x, y, zd, beta, acc);
+  }
+}
+
+// KKT gradient core y^(beta-2) (y - x) (diagnostics.py:51-54), formed per element so that the
+// side products accumulate the gradient itself instead of two sums that cancel
+template <int FBC>
+__device__ __forceinline__ float gcore32(float x, float y, float beta) {
+  const float d = y - x;
+  if (FBC == FBC_2) return d;
+  if (FBC == FBC_15) return d * rsqrt_fast(y);
+  const float r = rcp_fast(y);
+  if (FBC == FBC_1) return d * r;
+  if (FBC == FBC_0) return d * r * r;
+  return d * powf(y, beta - 2.f);
+}
+
 // Z for 8 elements; beta = 1.5 forms two lanes per instruction (FMUL2)
 template <int FBC>
 __device__ __forceinline__ void zpair8(const float* x, const float* y, float beta, float* zn,

@@ -67,24 +67,27 @@ __global__ void update_w(const T* __restrict__ base, const double* __restrict__ 
   }
 }
 
-// Column sums of an F x K matrix -> double K-vector.  One block of 256 threads per column:
-// thread t sums rows t, t + 256, ... in order, then a fixed shared-memory tree (deterministic).
+// Column sums of an F x K matrix -> double K-vector, one thread per column, rows added in
+// order: the order of numpy's sum over axis 0, so that the beta = 1 denominators (and the
+// exact-equality stop rule that can hang on their last bit) match the reference bit for bit.
+// Sixteen rows are loaded before any is added (the loads, not the adds, are the latency).
 template <typename T>
-__global__ void __launch_bounds__(256) col_sums(const T* __restrict__ M, int F, int K,
-                                                double* __restrict__ out, const RunState* st,
-                                                int slot) {
+__global__ void col_sums(const T* __restrict__ M, int F, int K, double* __restrict__ out,
+                         const RunState* st, int slot) {
   if (st && !iter_active(st, slot)) return;
-  const int k = blockIdx.x;
-  __shared__ double red[256];
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
   double s = 0.0;
-  for (int f = threadIdx.x; f < F; f += 256) s += double(M[(size_t)f * K + k]);
-  red[threadIdx.x] = s;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-    __syncthreads();
+  int f = 0;
+  for (; f + 16 <= F; f += 16) {
+    T v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = M[(size_t)(f + u) * K + k];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) s += double(v[u]);
   }
-  if (threadIdx.x == 0) out[k] = red[0];
+  for (; f < F; ++f) s += double(M[(size_t)f * K + k]);
+  out[k] = s;
 }
 
 // norms[k] = sqrt(sum_f W[f,k]^2); Wn = W / norms (solver.py:167-171).

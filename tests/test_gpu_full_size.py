@@ -44,6 +44,23 @@ def test_configs_2_3_full_size_match_oracle(cfg):
         assert np.all(got[1:] <= got[:-1] * (1 + 1e-6))
 
 
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_configs_2_3_tensor_core_pair_is_bitwise_repeatable(cfg):
+    """The tcgen05 pass pair (fused_tc3_kernel.cuh) at the full sizes of configs 2 and 3,
+    default kkt=True: three fits give bitwise the same trace (objective and KKT) and factors."""
+    F, N, K, beta = {2: (1024, 8192, 32, 2.0), 3: (1025, 16384, 20, 0.0)}[cfg]
+    v = (syn.config2 if cfg == 2 else syn.config3)().astype(np.float32)
+    w0, h0 = syn.uniform_init(F, N, K, seed=100 + K)
+    c = bn.SolverConfig(beta=beta, rank=K, algorithm="jmm", tol=1e-300, max_outer_iters=12)
+    runs = [bn.fit(v, c, init=(w0, h0), dtype="fp32") for _ in range(3)]
+    assert bn.get_context(0, "fp32").pass_info()[0] == "tcgen05"
+    t0 = [(r.objective, r.kkt_w, r.kkt_h) for r in runs[0].trace]
+    for other in runs[1:]:
+        assert [(r.objective, r.kkt_w, r.kkt_h) for r in other.trace] == t0
+        assert np.array_equal(other.factors.w, runs[0].factors.w)
+        assert np.array_equal(other.factors.h, runs[0].factors.h)
+
+
 def _objective_fp64(v, w, h, beta, chunk=1 << 18):
     """sum d_beta(v | w h) in fp64 on the device, column chunk by column chunk."""
     dev = torch.device("cuda:0")

@@ -1,8 +1,7 @@
-"""Parity sweep of the register-tiled SIMT fused pass (fs2::hpass + fs2::wpass, fp32) against
-the CPU oracle.
-
-The SIMT pair runs every fused shape outside the tcgen05 kernel's limits (F > 256 or K > 16,
-configs 2 and 3).  The sweep covers both K-tile instances (K <= 32 and 32 < K <= 64), odd and
+"""Parity sweep of the fused passes for the shapes outside the single-read tcgen05 kernel's
+limits (F > 256 or K > 16, configs 2 and 3) against the CPU oracle: the tcgen05 pass pair
+(fused_tc3_kernel.cuh, K <= 32) and the register-tiled SIMT pair (fs2::hpass + fs2::wpass,
+32 < K <= 64, and every shape with BNMF_TC3=0).  The sweep covers both K-tile instances (K <= 32 and 32 < K <= 64), odd and
 ragged K, F with a one-row last chunk (1025 = 16 x 64 + 1), column counts that are not a
 multiple of the 32-column step, every beta class (0, 1, 2 and the generic rule at 0.5 / 1.5),
 kappa > 0, JMM and BMM, and a TC-eligible shape forced onto the SIMT pair.  The gate is the
@@ -19,7 +18,7 @@ pytestmark = pytest.mark.gpu
 
 ITERS = 40
 SHAPES = [(300, 700, 20), (1025, 515, 33), (70, 203, 49), (130, 1000, 64), (257, 96, 1),
-          (520, 1100, 32)]
+          (520, 1100, 32), (200, 900, 27), (1025, 2100, 12)]
 BETAS = [0.0, 0.5, 1.0, 1.5, 2.0]
 
 
@@ -76,3 +75,22 @@ def test_simt_pass_forced_on_tc_shape(monkeypatch):
     r2 = _check(v, init, 1.5, 7, "jmm", 0.0)
     assert np.array_equal(r1.factors.w, r2.factors.w)
     assert np.array_equal(r1.factors.h, r2.factors.h)
+
+
+@pytest.mark.parametrize("shape", [(300, 700, 20), (257, 96, 1), (520, 1100, 32)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_simt_pair_on_the_tensor_core_shapes(shape):
+    """BNMF_TC3=0 keeps the K <= 32 shapes on the SIMT pair (the tcgen05 pass pair is the
+    default for them); both must hold the gate."""
+    import os
+    F, N, K = shape
+    v, init = _data(F, N, K)
+    os.environ["BNMF_TC3"] = "0"
+    try:
+        for beta in (0.0, 1.5):
+            _check(v, init, beta, K, "jmm", 0.0)
+            assert bn.get_context(0, "fp32").pass_info()[0] == "simt"
+    finally:
+        del os.environ["BNMF_TC3"]
+    _check(v, init, 1.0, K, "bmm", 0.0)
+    assert bn.get_context(0, "fp32").pass_info()[0] == "tcgen05"

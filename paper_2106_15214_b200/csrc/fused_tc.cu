@@ -85,6 +85,8 @@ static int env_cluster_cap() {
 
 static FusedState* g_last_tc = nullptr;
 
+constexpr int TC3_KKT_BLOCKS = 592;   // blocks (= partial sums) of the pair's H-side KKT finish
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -201,8 +203,10 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
     fs->s2_S = (io.N + fs->s2_seg - 1) / fs->s2_seg;
   }
   const char* force_simt = getenv("BNMF_FUSED_SIMT");
+  // BNMF_TC_PAIR=1: the pass pair also for the single-read kernel's shapes (A/B knob)
+  const char* force_pair = getenv("BNMF_TC_PAIR");
   fs->tc = fused_tc_shape_ok(io.F, io.K) && encode_fn() != nullptr &&
-           !(force_simt && force_simt[0] == '1');
+           !(force_simt && force_simt[0] == '1') && !(force_pair && force_pair[0] == '1');
   if (fs->tc) {
     const int nb = (io.N + ftc::BN - 1) / ftc::BN;
     fs->tc_smem = ftc::SMEM_BYTES;
@@ -255,7 +259,7 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
     FCK(cudaMemset(fs->prof, 0, np * sizeof(long long)));
     g_last_tc = fs;
   }
-  fs->kparts = std::max(gmax, (io.N + fs2::NC - 1) / fs2::NC);
+  fs->kparts = std::max(std::max(gmax, (io.N + fs2::NC - 1) / fs2::NC), TC3_KKT_BLOCKS);
   FCK(cudaMalloc(&fs->kpart, size_t(fs->kparts) * sizeof(double)));
   FCK(cudaMalloc(&fs->kcs, io.K * sizeof(double)));
   FCK(cudaMalloc(&fs->part, size_t(gmax) * 2 * fk * sizeof(double)));
@@ -360,6 +364,14 @@ static cudaError_t launch_tc3(FusedState* fs, const FusedArgs& a, const FusedIO&
                               int p_override) {
   const dim3 grid(fs->t3_gx, fs->t3_r);
   const int sm = int(ftc3::Lay<KP>::SMEM);
+  if (a.kkt == 3) {   // H-side KKT pass: grad_H partials, then |min(H~, grad_H)| per block
+    auto hk = ftc3::pass_tc3<FBC, true, KP, ftc3::MODE_H>;
+    cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    hk<<<grid, ftc3::NTHREADS3, sm, io.stream>>>(a, fs->mapV, fs->hpart, io.st, slot, p_override);
+    ftc3::tc3_kkt_h_finish<KP><<<TC3_KKT_BLOCKS, 256, 0, io.stream>>>(a, fs->hpart, fs->t3_r, io.st,
+                                                                      slot);
+    return cudaGetLastError();
+  }
   if (a.do_h && !a.kkt) {
     auto hk = ftc3::pass_tc3<FBC, true, KP, ftc3::MODE_H>;
     cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
@@ -542,7 +554,10 @@ static int enqueue_kkt(FusedState* fs, const FusedIO& io, int slot, std::string&
   wp.w[0] = fs->W2[0]; wp.w[1] = fs->W2[1];
   const size_t fk2 = size_t(2) * io.F * io.K;
   int nparts = fs->tc_grid;
-  if (!fs->tc) {   // SIMT pair and the tcgen05 pass pair: fs2::hpass in KKT mode
+  if (fs->tc3) {
+    a.kkt = 3;
+    nparts = TC3_KKT_BLOCKS;
+  } else if (!fs->tc) {   // SIMT pair: fs2::hpass in KKT mode
     nparts = (io.N + fs2::NC - 1) / fs2::NC;
     if (a.den_ones) {
       kkt_colsum<<<io.K, 256, 0, io.stream>>>(wp, io.F, io.K, fs->kcs, io.st, slot);

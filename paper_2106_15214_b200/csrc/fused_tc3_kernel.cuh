@@ -103,11 +103,16 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
   const int nblocks = (N + BN - 1) / BN;
   const int nb = gx < nblocks ? (nblocks - 1 - gx) / GX + 1 : 0;
   const int par = iter_parity(st, slot, p_override);
-  const float* Hsrc = MODE == MODE_H ? a.Hbuf[par ^ 1] : (a.do_h ? a.Hout[par] : a.Hbuf[par]);
+  // KKT passes (a.kkt): the gradient core g = y^(beta-2) (y - x) of the finished iterate
+  // (W~_p, H~_p) takes the place of Z_n and nothing that of Z_d, so that
+  //   MODE_W: AccW num = g H~_p^T = grad_W (into the slab's num half)
+  //   MODE_H: AccH num = W~_p^T g = grad_H (chi1 := W~_p; into hpart's num half)
+  const int kkt = a.kkt;
+  const float* Hsrc = (MODE == MODE_H && !kkt) ? a.Hbuf[par ^ 1] : (a.do_h ? a.Hout[par] : a.Hbuf[par]);
   const float* Wt = a.Wt2[par];
-  const float* Wa = a.algorithm == 0 ? a.Wt2[par ^ 1] : a.Wn;
-  const int den_ones = a.den_ones;
-  const int kkt = a.kkt;   // MODE_W only: grad_W = (y^(beta-2) (y - x)) H~_p^T into the slab's num half
+  const float* Wa = kkt ? Wt : (a.algorithm == 0 ? a.Wt2[par ^ 1] : a.Wn);
+  const float* C1g = kkt ? Wt : a.C1;
+  const int den_ones = kkt ? 1 : a.den_ones;   // no denominator products in the KKT passes
   const float kappa = float(a.sc.kappa), beta = float(a.sc.beta);
   auto col0 = [&](int blk) { return (gx + blk * GX) * BN; };
 
@@ -141,7 +146,7 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
       v = ok ? Wa[gi] : 0.f; hi = tf32_hi(v);
       sts_f32(sb + L::OFF_A + L::core(fl, k), hi);
       sts_f32(sb + L::OFF_A + L::OPB + L::core(fl, k), v - hi);
-      v = ok ? a.C1[gi] : 0.f; hi = tf32_hi(v);
+      v = ok ? C1g[gi] : 0.f; hi = tf32_hi(v);
       sts_f32(sb + L::OFF_B + coreT_off(k, fl), hi);
       sts_f32(sb + L::OFF_B + coreT_off(k + KP, fl), v - hi);
       v = ok ? a.C2[gi] : 0.f; hi = tf32_hi(v);
@@ -310,13 +315,22 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
 #pragma unroll
               for (int i = 0; i < 8; ++i) y[8 * s4 + i] += kappa;
             }
-            zpair8<FBC>(x + 8 * s4, y + 8 * s4, beta, zn, zd);
-            if (!full) {
+            if (kkt) {
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
                 const bool ok = nok && (32 * j + 8 * s4 + i < FTr);
-                zn[i] = ok ? zn[i] : 0.f;
-                zd[i] = ok ? zd[i] : 0.f;
+                zn[i] = ok ? gcore32<FBC>(x[8 * s4 + i], y[8 * s4 + i], beta) : 0.f;
+                zd[i] = 0.f;
+              }
+            } else {
+              zpair8<FBC>(x + 8 * s4, y + 8 * s4, beta, zn, zd);
+              if (!full) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const bool ok = nok && (32 * j + 8 * s4 + i < FTr);
+                  zn[i] = ok ? zn[i] : 0.f;
+                  zd[i] = ok ? zd[i] : 0.f;
+                }
               }
             }
             if (s4 == 0) wait_zfree();
@@ -605,6 +619,33 @@ __global__ void tc3_h_finish(FusedArgs a, const float* __restrict__ hpart, int R
     const double hp = double(Hprev[t]) * apply_exponent<double>(ratio, a.sc.gamma);
     Hnew[t] = float(hp * a.norms[k]);
   }
+}
+
+// res_H partial sums of the H-side KKT pass: |min(H~_p, grad_H)| with grad_H the slices'
+// partial sums added in order; one partial per block (fixed tree)
+template <int KP>
+__global__ void __launch_bounds__(256) tc3_kkt_h_finish(FusedArgs a, const float* __restrict__ hpart,
+                                                        int R, const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  const float* Hp = a.Hbuf[iter_parity(st, slot, -1)];
+  const size_t total = size_t(a.N) * a.K;
+  __shared__ double red[256];
+  double s = 0.0;
+  for (size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x; t < total;
+       t += size_t(gridDim.x) * blockDim.x) {
+    const size_t n = t / a.K;
+    const int k = int(t - n * a.K);
+    float g = 0.f;
+    for (int r = 0; r < R; ++r) g += hpart[(size_t(r) * a.N + n) * (2 * KP) + k];
+    s += fabs(fmin(double(Hp[t]), double(g)));
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.opart[blockIdx.x] = red[0];
 }
 
 }  // namespace ftc3

@@ -340,6 +340,8 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
     const bool rows_full = FTr == 32 * SH;
     const bool fok = row < FTr;
     double obj = 0.0;
+    float pc[PHI_TERMS];
+    if (FBC == FBC_GEN) phi_coeffs(beta, pc);
     int m = 0;   // own items done (phase counter of this team's buffers)
 
     // Vt tile of the item -> registers (buffer handed back), then wait until the side
@@ -449,8 +451,8 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
             float o0 = 0.f, o1 = 0.f;
 #pragma unroll
             for (int i = 0; i < 8; i += 2) {
-              z_and_obj<FBC>(xx[i], yy[i], 0.f, beta, zn[i], zd[i], o0);
-              z_and_obj<FBC>(xx[i + 1], yy[i + 1], 0.f, beta, zn[i + 1], zd[i + 1], o1);
+              z_and_obj<FBC>(xx[i], yy[i], 0.f, beta, zn[i], zd[i], o0, pc);
+              z_and_obj<FBC>(xx[i + 1], yy[i + 1], 0.f, beta, zn[i + 1], zd[i + 1], o1, pc);
             }
             objb += o0 + o1;
           } else {
@@ -459,7 +461,7 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
             for (int i = 0; i < 8; ++i) {
               const bool ok = fok && (n0 + 32 * idx + c0 + 8 * s4 + i < N);
               float t = 0.f;
-              z_and_obj<FBC>(xx[i], yy[i], 0.f, beta, zn[i], zd[i], t);
+              z_and_obj<FBC>(xx[i], yy[i], 0.f, beta, zn[i], zd[i], t, pc);
               zn[i] = ok ? zn[i] : 0.f;
               zd[i] = ok ? zd[i] : 0.f;
               o0 += ok ? t : 0.f;

@@ -261,6 +261,8 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
     const bool fok = row < FTr;
     double obj = 0.0;
     int m = 0, c = 0;
+    float pc[PHI_TERMS];
+    if (FBC == FBC_GEN) phi_coeffs(beta, pc);
     int s_cur = 0;
     uint32_t p_cur = 0;
     auto slot_of = [&](int j, uint32_t& ph) {
@@ -388,8 +390,8 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
               float o0 = 0.f, o1 = 0.f;
 #pragma unroll
               for (int i = 0; i < 8; i += 2) {
-                z_and_obj<FBC>(xx[i], yy[i], 0.f, beta, zn[i], zd[i], o0);
-                z_and_obj<FBC>(xx[i + 1], yy[i + 1], 0.f, beta, zn[i + 1], zd[i + 1], o1);
+                z_and_obj<FBC>(xx[i], yy[i], 0.f, beta, zn[i], zd[i], o0, pc);
+                z_and_obj<FBC>(xx[i + 1], yy[i + 1], 0.f, beta, zn[i + 1], zd[i + 1], o1, pc);
               }
               objb += o0 + o1;
             } else {
@@ -398,7 +400,7 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
               for (int i = 0; i < 8; ++i) {
                 const bool ok = fok && (n0 + 32 * u + 8 * s4 + i < N);
                 float t = 0.f;
-                z_and_obj<FBC>(xx[i], yy[i], 0.f, beta, zn[i], zd[i], t);
+                z_and_obj<FBC>(xx[i], yy[i], 0.f, beta, zn[i], zd[i], t, pc);
                 zn[i] = ok ? zn[i] : 0.f;
                 zd[i] = ok ? zd[i] : 0.f;
                 o0 += ok ? t : 0.f;

@@ -144,9 +144,21 @@ __device__ __forceinline__ void dacc(float x, float y, float zd, float beta, flo
 // forms; divergence32 gets it from an IEEE division and a 14-term series, which made the W items
 // of these classes ~10x the H items.  Here u = (x - y) rcp(y) with the reciprocal Z needs anyway,
 // an 8-term Horner series for |u| < 1/8 (truncation < 2^-24 of the term) and the MUFU log beyond.
+// series coefficients of phi(u) = [(1 + u)^b - 1 - b u] / (b (b - 1)) = sum_{j >= 2} t_j u^j,
+// t_2 = 1/2, t_{j+1} = t_j (b - j) / (j + 1): computed once per thread (generic beta)
+constexpr int PHI_TERMS = 12;
+__device__ __forceinline__ void phi_coeffs(float b, float* pc) {
+  float t = 0.5f;
+#pragma unroll
+  for (int j = 2; j < 2 + PHI_TERMS; ++j) {
+    pc[j - 2] = t;
+    t = t * (b - float(j)) / float(j + 1);
+  }
+}
+
 template <int FBC>
 __device__ __forceinline__ void z_and_obj(float x, float y, float zd_in, float beta, float& zn,
-                                          float& zd, float& acc) {
+                                          float& zd, float& acc, const float* pc = nullptr) {
   (void)zd_in;
   if (FBC == FBC_0) {
     const float r = rcp_fast(y);
@@ -191,6 +203,24 @@ __device__ __forceinline__ void z_and_obj(float x, float y, float zd_in, float b
       d = y;
     } else {
       d = x * __logf(x * r) - x + y;
+    }
+    acc += d;
+  } else if (FBC == FBC_GEN && pc != nullptr) {
+    // one powf: a = y^(beta-2) gives Z, y^(beta-1) = a y and y^beta = a y^2; the objective is
+    // y^beta phi(u) by its series (Horner, coefficients in pc) for |u| < 1/4, the three-term
+    // form (one more powf) beyond
+    const float a = powf(y, beta - 2.f);
+    zn = x * a;
+    zd = a * y;
+    const float u = (x - y) * rcp_fast(y), yb = zd * y;
+    float d;
+    if (fabsf(u) < 0.25f) {
+      float p = pc[PHI_TERMS - 1];
+#pragma unroll
+      for (int j = PHI_TERMS - 2; j >= 0; --j) p = fmaf(p, u, pc[j]);
+      d = yb * p * u * u;
+    } else {
+      d = powf(x, beta) / (beta * (beta - 1.f)) + yb / beta - x * zd / (beta - 1.f);
     }
     acc += d;
   } else {
@@ -792,6 +822,8 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
     };
 
     const bool rows_full = FTr == 32 * SH;
+    float pc[PHI_TERMS];
+    if (FBC == FBC_GEN) phi_coeffs(beta, pc);
     int c = 0;   // item counter (Vt / Z buffer c & 1)
     float objb = 0.f;   // objective of the current block (fp32, 32 terms per thread)
     // Vt tile of item c -> registers; the buffer is handed back right away
@@ -894,10 +926,8 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
 #pragma unroll
         for (int i = 0; i < 8; i += 2) {
           const float y0 = KAPPA ? y[i] + kappa : y[i], y1 = KAPPA ? y[i + 1] + kappa : y[i + 1];
-          zpair<FBC>(x[i], y0, beta, zn[i], zd[i]);
-          zpair<FBC>(x[i + 1], y1, beta, zn[i + 1], zd[i + 1]);
-          dacc<FBC>(x[i], y0, zd[i], beta, o0);
-          dacc<FBC>(x[i + 1], y1, zd[i + 1], beta, o1);
+          z_and_obj<FBC>(x[i], y0, 0.f, beta, zn[i], zd[i], o0, pc);
+          z_and_obj<FBC>(x[i + 1], y1, 0.f, beta, zn[i + 1], zd[i + 1], o1, pc);
         }
         objb += o0 + o1;
       } else {
@@ -906,10 +936,9 @@ fused_pass_tc(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const float yy = KAPPA ? y[i] + kappa : y[i];
-          zpair<FBC>(x[i], yy, beta, zn[i], zd[i]);
           const bool ok = fok && (n0 + 32 * idx + 8 * g + i < N);
           float t = 0.f;
-          dacc<FBC>(x[i], yy, zd[i], beta, t);
+          z_and_obj<FBC>(x[i], yy, 0.f, beta, zn[i], zd[i], t, pc);
           zn[i] = ok ? zn[i] : 0.f;
           zd[i] = ok ? zd[i] : 0.f;
           o0 += ok ? t : 0.f;

@@ -78,6 +78,12 @@ static bool tc3_wanted(int K) {
   return K <= 32 && !(e && e[0] == '0') && !(f && f[0] == '1');
 }
 
+// BNMF_TC_PAIR=1: the pass pair also for the single-read kernel's shapes (A/B knob)
+static bool env_force_pair() {
+  const char* e = getenv("BNMF_TC_PAIR");
+  return e && e[0] == '1';
+}
+
 static int env_cluster_cap() {
   const char* c = getenv("BNMF_TC_MAX_CLUSTERS");
   return c ? std::max(0, atoi(c)) : 0;
@@ -203,10 +209,8 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
     fs->s2_S = (io.N + fs->s2_seg - 1) / fs->s2_seg;
   }
   const char* force_simt = getenv("BNMF_FUSED_SIMT");
-  // BNMF_TC_PAIR=1: the pass pair also for the single-read kernel's shapes (A/B knob)
-  const char* force_pair = getenv("BNMF_TC_PAIR");
   fs->tc = fused_tc_shape_ok(io.F, io.K) && encode_fn() != nullptr &&
-           !(force_simt && force_simt[0] == '1') && !(force_pair && force_pair[0] == '1');
+           !(force_simt && force_simt[0] == '1') && !env_force_pair();
   if (fs->tc) {
     const int nb = (io.N + ftc::BN - 1) / ftc::BN;
     fs->tc_smem = ftc::SMEM_BYTES;
@@ -606,7 +610,7 @@ static int enqueue_kkt(FusedState* fs, const FusedIO& io, int slot, std::string&
 
 bool fused_shape_matches(const FusedState* fs, int F, int N, int K) {
   return fs && fs->F == F && fs->N == N && fs->K == K && (!fs->tc || (fs->cap == env_cluster_cap() && fs->v1 == env_tc_v1())) &&
-         (fs->tc || fs->tc3 == tc3_wanted(K));
+         (fs->tc || fs->tc3 == tc3_wanted(K)) && (!fs->tc || !env_force_pair());
 }
 
 void fused_info(const FusedState* fs, int* out4) {

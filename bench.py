@@ -423,10 +423,10 @@ def main():
                                 kappa=kappa, max_outer_iters=max(1, args.warmup))
         bn.fit(vp, cfg_w, init=(w0, h0), dtype=c["dtype"], schedule=args.schedule,
                sharded=world > 1)
-        # median of three timed calls: the host side (fresh fp64 result arrays, pageable
-        # copies of the init and factors) varies by +-30 % from call to call
+        # median of five timed calls: the host side (fresh fp64 result arrays, pageable
+        # copies of the init and factors) varies by +-30 % from call to call, with outliers
         tes = []
-        for _rep in range(3):
+        for _rep in range(5):
             if world > 1:
                 torch.distributed.barrier()
             t0 = time.perf_counter()
@@ -443,7 +443,7 @@ def main():
         e2e = {"value": args.steps / te, "unit": "iterations/s",
                "h2d_bytes_per_step": int(h2d * world / args.steps),
                "d2h_bytes_per_step": int(d2h * world / args.steps),
-               "note": "median of 3 default fit() calls (kkt=True) on pinned host V after one "
+               "note": "median of 5 default fit() calls (kkt=True) on pinned host V after one "
                        f"untimed warm-up call; each: upload, domain checks, {args.steps} "
                        "iterations with their KKT passes, download of W, H and trace",
                "calls_s": [round(t, 4) for t in tes]}

@@ -51,6 +51,7 @@ struct FusedState {
   size_t tc_smem = 0;
   CUtensorMap mapV;
   long long* prof = nullptr;   // BNMF_TC_PROF=1: wait-cycle counters [grid][48]
+  size_t prof_n = 0;
   int cap = 0;                 // BNMF_TC_MAX_CLUSTERS at creation (test knob)
   bool v1 = true;              // false with BNMF_TC_V2=1 (second-generation kernel, A/B knob)
   // tcgen05 pass pair over a (column group, 128-row slice) grid: F > 256 or 16 < K <= 32
@@ -257,8 +258,9 @@ int fused_create(FusedState** out, const FusedIO& io, std::string& err) {
   int gmax = std::max(std::max(fs->tc_grid, fs->s2_S), fs->t3_gx);
   const int gobj = std::max(std::max(gmax, fs->s2_S * fs->s2_rc), fs->t3_gx * fs->t3_r);
   const char* prof_env = getenv("BNMF_TC_PROF");
-  if (fs->tc && prof_env && prof_env[0] == '1') {
-    const size_t np = size_t(fs->tc_grid) * 288 + 3 * 4096;
+  if ((fs->tc || fs->tc3) && prof_env && prof_env[0] == '1') {
+    const size_t np = size_t(std::max(fs->tc_grid, fs->t3_gx * fs->t3_r)) * 288 + 3 * 4096;
+    fs->prof_n = np;
     FCK(cudaMalloc(&fs->prof, np * sizeof(long long)));
     FCK(cudaMemset(fs->prof, 0, np * sizeof(long long)));
     g_last_tc = fs;
@@ -371,7 +373,7 @@ static cudaError_t launch_tc3(FusedState* fs, const FusedArgs& a, const FusedIO&
   if (a.kkt == 3) {   // H-side KKT pass: grad_H partials, then |min(H~, grad_H)| per block
     auto hk = ftc3::pass_tc3<FBC, true, KP, ftc3::MODE_H>;
     cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    hk<<<grid, ftc3::NTHREADS3, sm, io.stream>>>(a, fs->mapV, fs->hpart, io.st, slot, p_override);
+    hk<<<grid, ftc3::threads_of(FBC), sm, io.stream>>>(a, fs->mapV, fs->hpart, io.st, slot, p_override);
     ftc3::tc3_kkt_h_finish<KP><<<TC3_KKT_BLOCKS, 256, 0, io.stream>>>(a, fs->hpart, fs->t3_r, io.st,
                                                                       slot);
     return cudaGetLastError();
@@ -379,14 +381,14 @@ static cudaError_t launch_tc3(FusedState* fs, const FusedArgs& a, const FusedIO&
   if (a.do_h && !a.kkt) {
     auto hk = ftc3::pass_tc3<FBC, true, KP, ftc3::MODE_H>;
     cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    hk<<<grid, ftc3::NTHREADS3, sm, io.stream>>>(a, fs->mapV, fs->hpart, io.st, slot, p_override);
+    hk<<<grid, ftc3::threads_of(FBC), sm, io.stream>>>(a, fs->mapV, fs->hpart, io.st, slot, p_override);
     const size_t nk = size_t(io.N) * io.K;
     ftc3::tc3_h_finish<KP><<<int(std::min<size_t>((nk + 255) / 256, 148 * 8)), 256, 0, io.stream>>>(
         a, fs->hpart, fs->t3_r, io.st, slot, p_override);
   }
   auto wk = ftc3::pass_tc3<FBC, true, KP, ftc3::MODE_W>;
   cudaFuncSetAttribute(wk, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  wk<<<grid, ftc3::NTHREADS3, sm, io.stream>>>(a, fs->mapV, fs->hpart, io.st, slot, p_override);
+  wk<<<grid, ftc3::threads_of(FBC), sm, io.stream>>>(a, fs->mapV, fs->hpart, io.st, slot, p_override);
   return cudaGetLastError();
 }
 
@@ -684,7 +686,7 @@ int fused_export(FusedState* fs, const FusedIO& io, std::string& err) {
 extern "C" int bnmf_tc_prof_read(long long* out, int max) {
   bnmf::FusedState* fs = bnmf::g_last_tc;
   if (!fs || !fs->prof) return 0;
-  int n = std::min(max, fs->tc_grid * 288 + 3 * 4096);
+  int n = std::min(max, int(fs->prof_n));
   if (cudaMemcpy(out, fs->prof, size_t(n) * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
     return -1;
   return n;

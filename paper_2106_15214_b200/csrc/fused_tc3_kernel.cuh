@@ -31,10 +31,22 @@ using namespace bnmf::ftc;
 using bnmf::ftc2::tmem_ld32;
 
 constexpr int MODE_H = 0, MODE_W = 1;
-constexpr int TW = 4;                      // warps per item team
-constexpr int W_TMA = 0, W_VT = 1, W_SIDE = 2, W_TEAM0 = 3, W_UTEAM = W_TEAM0 + 2 * TW;
-constexpr int NWARPS3 = W_UTEAM + 4;       // 15
-constexpr int NTHREADS3 = 32 * NWARPS3;
+constexpr int TW = 4;                      // warps per item team (one per TMEM lane quadrant)
+// Item teams and item width.  TMEM holds 64 Vt columns and 256 Z columns for the items in
+// flight: 2 teams x 32-column items or 4 teams x 16-column items.  Four teams double the warps
+// that overlap the MUFU / FMA / ALU work of different items (a lone warp issues one
+// instruction every ~2.7 cycles) for 6 more small Vt MMAs per 32 columns: that pays for the
+// classes with a long objective (beta = 0, 1, generic: config 3 0.161 -> 0.140 ms) and costs
+// for the short ones (beta = 2, 1.5: config 2 0.077 -> 0.083 ms), so the class picks.
+__host__ __device__ constexpr int teams_of(int fbc) {
+#ifdef BNMF_TC3_NT
+  return BNMF_TC3_NT;
+#else
+  return (fbc == FBC_2 || fbc == FBC_15) ? 2 : 4;
+#endif
+}
+constexpr int W_TMA = 0, W_VT = 1, W_SIDE = 2, W_TEAM0 = 3;
+__host__ __device__ constexpr int threads_of(int fbc) { return 32 * (W_TEAM0 + teams_of(fbc) * TW + 4); }
 
 template <int KP>
 struct Lay {
@@ -71,11 +83,18 @@ __device__ __forceinline__ void issue_vt3(uint32_t dcol, uint32_t a_hi, uint32_t
 }
 
 template <int FBC, bool KAPPA, int KP, int MODE>
-__global__ void __launch_bounds__(NTHREADS3, 1)
+__global__ void __launch_bounds__(threads_of(FBC), 1)
 pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restrict__ hpart,
          const RunState* st, int slot, int p_override) {
   if (p_override < 0 && !iter_active(st, slot)) return;
   using L = Lay<KP>;
+  constexpr int NT = teams_of(FBC);          // item teams
+  constexpr int IW = 64 / NT;                // columns of an item
+  constexpr int NCH = IW / 8;                // Z k-steps of an item
+  constexpr int HIT = 32 / IW;               // H items per V stage
+  constexpr int WIT = BN / IW;               // W items per block
+  constexpr int W_UTEAM = W_TEAM0 + NT * TW;
+  constexpr int NWARPS3 = W_UTEAM + 4;       // 15 or 23
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
@@ -83,18 +102,28 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* bar_full = bars;           // [NSTAGE]
   uint64_t* bar_empty = bars + 8;      // [NSTAGE]
-  uint64_t* bar_dfull = bars + 16;     // [2]
-  uint64_t* bar_dfree = bars + 18;     // [2]
-  uint64_t* bar_zfull = bars + 20;     // [2]
-  uint64_t* bar_zfree = bars + 22;     // [2]
-  uint64_t* bar_op = bars + 24;        // the block's A operand (MODE_H) / B operands (MODE_W) are in place
-  uint64_t* bar_opfree = bars + 25;    // the block's Vt tiles (MODE_H) / W-side products (MODE_W) retired
-  uint64_t* bar_acc = bars + 26;       // Acc complete (MODE_H: every block; MODE_W: every fold)
-  uint64_t* bar_accfree = bars + 27;   // Acc read out
+  uint64_t* bar_dfull = bars + 16;     // [NT]
+  uint64_t* bar_dfree = bars + 20;     // [NT]
+  uint64_t* bar_zfull = bars + 24;     // [NT]
+  uint64_t* bar_zfree = bars + 28;     // [NT]
+  uint64_t* bar_op = bars + 32;        // the block's A operand (MODE_H) / B operands (MODE_W) are in place
+  uint64_t* bar_opfree = bars + 33;    // the block's Vt tiles (MODE_H) / W-side products (MODE_W) retired
+  uint64_t* bar_acc = bars + 34;       // Acc complete (MODE_H: every block; MODE_W: every fold)
+  uint64_t* bar_accfree = bars + 35;   // Acc read out
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 40);
-  __shared__ double s_red[2 * TW];
+  __shared__ double s_red[NT * TW];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // optional wait-cycle counters (-DBNMF_TC_PROF): [CTA][warp][12] like fused_tc2_kernel.cuh
+#ifdef BNMF_TC_PROF
+  long long pc_[12];
+#pragma unroll
+  for (int i = 0; i < 12; ++i) pc_[i] = 0;
+  const long long t_start_ = clock64();
+#define W3(call, cat) do { const long long t0_ = clock64(); call; pc_[cat] += clock64() - t0_; } while (0)
+#else
+#define W3(call, cat) call
+#endif
   const int F = a.F, N = a.N, K = a.K;
   const int row0 = blockIdx.y * FR;
   const int FTr = min(FR, F - row0);
@@ -119,9 +148,9 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&bar_full[s], 1);
-      mbar_init(&bar_empty[s], MODE == MODE_H ? TW : 2 * TW);
+      mbar_init(&bar_empty[s], MODE == MODE_H ? HIT * TW : NT * TW);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NT; ++b) {
       mbar_init(&bar_dfull[b], 1);
       mbar_init(&bar_dfree[b], TW);
       mbar_init(&bar_zfull[b], TW);
@@ -159,7 +188,7 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
-  const int nit = MODE == MODE_H ? SH : SW;   // items per block
+  const int nit = MODE == MODE_H ? SH * HIT : WIT;   // items per block
 
   if (warp == W_TMA) {
     if (lane == 0) {
@@ -168,7 +197,7 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
       for (int bi = 0; bi < nb; ++bi) {
         const int n0 = col0(bi);
         for (int j = 0; j < SH; ++j) {
-          mbar_wait(&bar_empty[s], ph ^ 1u);
+          W3(mbar_wait(&bar_empty[s], ph ^ 1u), 0);
           mbar_expect_tx(&bar_full[s], STAGE_BYTES);
           tma_load_2d(smem + s * STAGE_BYTES, &mapV, &bar_full[s], n0, row0 + 32 * j);
           if (++s == NSTAGE) { s = 0; ph ^= 1u; }
@@ -177,20 +206,21 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
     }
   } else if (warp == W_VT) {
     // ======================= Vt issuer =======================================
-    const uint32_t id32 = idesc_tf32(128, 32, 0, 0);
+    const uint32_t id_vt = idesc_tf32(128, IW, 0, 0);
     const uint64_t d_b = sdesc(sb + L::OFF_A, 128, L::CORE_SBO);
     int c = 0;
     for (int bi = 0; bi < nb; ++bi) {
-      mbar_wait(bar_op, bi & 1);
+      W3(mbar_wait(bar_op, bi & 1), 0);
       for (int j = 0; j < nit; ++j) {
-        const int b = c & 1, m = c >> 1;
+        const int b = c & (NT - 1), m = c / NT;
         ++c;
-        if (m > 0) mbar_wait(&bar_dfree[b], (m - 1) & 1);
+        if (m > 0) W3(mbar_wait(&bar_dfree[b], (m - 1) & 1), 1);
         tc_fence_after();
         if (elect_one()) {
-          // rows 32 j.. of the B tile: 4 eight-row groups further
-          issue_vt3<KP>(tmem + TM_D + 32 * b, tmem + L::TM_OP, tmem + L::TM_OP + KP,
-                        dplus(d_b, j * 4 * L::CORE_SBO), dplus(d_b, j * 4 * L::CORE_SBO + L::OPB), id32);
+          // rows IW j.. of the B tile: IW / 8 eight-row groups per item
+          issue_vt3<KP>(tmem + TM_D + IW * b, tmem + L::TM_OP, tmem + L::TM_OP + KP,
+                        dplus(d_b, j * (IW / 8) * L::CORE_SBO),
+                        dplus(d_b, j * (IW / 8) * L::CORE_SBO + L::OPB), id_vt);
           mma_commit(&bar_dfull[b]);
           if (MODE == MODE_H && j == nit - 1) mma_commit(bar_opfree);
         }
@@ -206,7 +236,7 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
     const uint64_t d_b2 = sdesc(sb + L::OFF_C, 128, 4096);
     auto side = [&](uint32_t acc, uint32_t z, uint64_t bdesc, uint32_t kstride, bool fresh) {
 #pragma unroll
-      for (int s = 0; s < 4; ++s) {
+      for (int s = 0; s < NCH; ++s) {
         mma_ts(acc, z + 32 * s, dplus(bdesc, kstride * s), id_hi, (fresh && s == 0) ? 0u : 1u);
         mma_ts(acc, z + 32 * s + 8, dplus(bdesc, kstride * s), id_lo, 1u);
       }
@@ -214,27 +244,30 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
     int c = 0, nfold = 0;
     for (int bi = 0; bi < nb; ++bi) {
       for (int j = 0; j < nit; ++j) {
-        const int b = c & 1, m = c >> 1;
+        const int b = c & (NT - 1), m = c / NT;
         ++c;
-        const uint32_t zb = tmem + TM_Z + 128 * b;
-        mbar_wait(&bar_zfull[b], m & 1);
+        const uint32_t zb = tmem + TM_Z + 4 * IW * b;
+        W3(mbar_wait(&bar_zfull[b], m & 1), 0);
         bool fresh;
         if (MODE == MODE_H) {
           fresh = j == 0;
-          if (fresh && bi > 0) mbar_wait(bar_accfree, (bi - 1) & 1);
+          if (fresh && bi > 0) W3(mbar_wait(bar_accfree, (bi - 1) & 1), 1);
         } else {
           fresh = (bi % FOLD) == 0 && j == 0;
-          if (fresh && bi > 0) { mbar_wait(bar_accfree, nfold & 1); ++nfold; }
+          if (fresh && bi > 0) { W3(mbar_wait(bar_accfree, nfold & 1), 1); ++nfold; }
         }
         tc_fence_after();
+#ifdef BNMF_TC_PROF
+        const long long ti_ = clock64();
+#endif
         if (elect_one()) {
           if (MODE == MODE_H) {
-            side(tmem + L::TM_ACC, zb, dplus(d_b1, j * 1024), 256, fresh);
-            if (!den_ones) side(tmem + L::TM_ACC + 2 * KP, zb + 16, dplus(d_b2, j * 1024), 256, fresh);
+            side(tmem + L::TM_ACC, zb, dplus(d_b1, j * IW * 32), 256, fresh);
+            if (!den_ones) side(tmem + L::TM_ACC + 2 * KP, zb + 16, dplus(d_b2, j * IW * 32), 256, fresh);
             mma_commit(&bar_zfree[b]);
             if (j == nit - 1) mma_commit(bar_acc);
           } else {
-            const uint64_t bh = dplus(d_b1, j * 8 * HNT_LBO);
+            const uint64_t bh = dplus(d_b1, j * (IW / 4) * HNT_LBO);
             side(tmem + L::TM_ACC, zb, bh, 2 * HNT_LBO, fresh);
             if (!kkt) side(tmem + L::TM_ACC + 2 * KP, zb + 16, bh, 2 * HNT_LBO, fresh);
             mma_commit(&bar_zfree[b]);
@@ -245,6 +278,9 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
           }
         }
         __syncwarp();
+#ifdef BNMF_TC_PROF
+        pc_[2] += clock64() - ti_;
+#endif
       }
     }
   } else if (warp < W_UTEAM) {
@@ -253,8 +289,8 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
     const int q = warp & 3;
     const int row = 32 * q + lane;
     const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16);
-    const uint32_t dcol = lane_base + TM_D + 32 * team;
-    const uint32_t zcol = lane_base + TM_Z + 128 * team;
+    const uint32_t dcol = lane_base + TM_D + IW * team;
+    const uint32_t zcol = lane_base + TM_Z + 4 * IW * team;
     const uint32_t dfull_a = smem_u32(&bar_dfull[team]), dfree_a = smem_u32(&bar_dfree[team]);
     const uint32_t zfull_a = smem_u32(&bar_zfull[team]), zfree_a = smem_u32(&bar_zfree[team]);
     const uint32_t full_a = smem_u32(bar_full), empty_a = smem_u32(bar_empty);
@@ -272,16 +308,17 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
       return s;
     };
     auto take_tile = [&](float* y) {
-      mbar_wait_a(dfull_a, m & 1);
+      W3(mbar_wait_a(dfull_a, m & 1), 0);
       tc_fence_after();
-      tmem_ld32(dcol, y);
+      if (IW == 32) tmem_ld32(dcol, y);
+      else tmem_ld16(dcol, y);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_a(dfree_a);
     };
     auto wait_zfree = [&]() {
       if (m > 0) {
-        mbar_wait_a(zfree_a, (m - 1) & 1);
+        W3(mbar_wait_a(zfree_a, (m - 1) & 1), 1);
         tc_fence_after();
       }
     };
@@ -295,23 +332,24 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
     for (int bi = 0; bi < nb; ++bi) {
       const int n0 = col0(bi);
       if (MODE == MODE_H) {
-        for (int j = 0; j < SH; ++j) {
-          const bool mine = (c & 1) == team;
+        for (int it = 0; it < SH * HIT; ++it) {
+          const bool mine = (c & (NT - 1)) == team;
           ++c;
           if (!mine) continue;
-          // ---------- H item: rows row0 + 32 j + [0, 32) of column n0 + row ----------
+          // ---------- H item: rows row0 + r0 + [0, IW) of column n0 + row ----------
+          const int j = it / HIT, r0 = IW * it;
           uint32_t ph;
           const int s = slot_of(j, ph);
-          float x[32], y[32];
-          mbar_wait_a(full_a + 8 * s, ph);
-          const uint32_t xa = sb + s * STAGE_BYTES + row * 4;
+          float x[IW], y[IW];
+          W3(mbar_wait_a(full_a + 8 * s, ph), 2);
+          const uint32_t xa = sb + s * STAGE_BYTES + (r0 - 32 * j) * VROWB + row * 4;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) x[i] = lds_f32(xa + i * VROWB);
+          for (int i = 0; i < IW; ++i) x[i] = lds_f32(xa + i * VROWB);
           take_tile(y);
-          const bool full = n0 + BN <= N && 32 * j + 32 <= FTr;
+          const bool full = n0 + BN <= N && r0 + IW <= FTr;
           const bool nok = n0 + row < N;
 #pragma unroll
-          for (int s4 = 0; s4 < 4; ++s4) {
+          for (int s4 = 0; s4 < NCH; ++s4) {
             float zn[8], zd[8];
             if (KAPPA) {
 #pragma unroll
@@ -320,7 +358,7 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
             if (kkt) {
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                const bool ok = nok && (32 * j + 8 * s4 + i < FTr);
+                const bool ok = nok && (r0 + 8 * s4 + i < FTr);
                 zn[i] = ok ? gcore32<FBC>(x[8 * s4 + i], y[8 * s4 + i], beta) : 0.f;
                 zd[i] = 0.f;
               }
@@ -329,7 +367,7 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
               if (!full) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                  const bool ok = nok && (32 * j + 8 * s4 + i < FTr);
+                  const bool ok = nok && (r0 + 8 * s4 + i < FTr);
                   zn[i] = ok ? zn[i] : 0.f;
                   zd[i] = ok ? zd[i] : 0.f;
                 }
@@ -347,30 +385,30 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
         if (q < SH) {
           uint32_t ph;
           const int s = slot_of(q, ph);
-          mbar_wait_a(full_a + 8 * s, ph);
+          W3(mbar_wait_a(full_a + 8 * s, ph), 2);
           xrow = sb + s * STAGE_BYTES + lane * VROWB;
         }
-        for (int u = 0; u < SW; ++u) {
-          const bool mine = (c & 1) == team;
+        for (int u = 0; u < WIT; ++u) {
+          const bool mine = (c & (NT - 1)) == team;
           ++c;
           if (!mine) continue;
-          // ---------- W item: row row0 + row, columns n0 + 32 u + [0, 32) ----------
-          float x[32], y[32];
+          // ---------- W item: row row0 + row, columns n0 + IW u + [0, IW) ----------
+          float x[IW], y[IW];
           if (q < SH) {
 #pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-              const float4 v = lds_f128(xrow + 128 * u + 4 * i);
+            for (int i = 0; i < IW; i += 4) {
+              const float4 v = lds_f128(xrow + 4 * IW * u + 4 * i);
               x[i] = v.x; x[i + 1] = v.y; x[i + 2] = v.z; x[i + 3] = v.w;
             }
           } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) x[i] = 0.f;
+            for (int i = 0; i < IW; ++i) x[i] = 0.f;
           }
           take_tile(y);
           const bool full = n0 + BN <= N && fok;
           float objb = 0.f;
 #pragma unroll
-          for (int s4 = 0; s4 < 4; ++s4) {
+          for (int s4 = 0; s4 < NCH; ++s4) {
             float zn[8], zd[8];
             float* yy = y + 8 * s4;
             const float* xx = x + 8 * s4;
@@ -382,7 +420,7 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
               // KKT pass: the gradient core in place of Z_n, nothing in place of Z_d
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                const bool ok = fok && (n0 + 32 * u + 8 * s4 + i < N);
+                const bool ok = fok && (n0 + IW * u + 8 * s4 + i < N);
                 zn[i] = ok ? gcore32<FBC>(xx[i], yy[i], beta) : 0.f;
                 zd[i] = 0.f;
               }
@@ -398,7 +436,7 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
               float o0 = 0.f;
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                const bool ok = fok && (n0 + 32 * u + 8 * s4 + i < N);
+                const bool ok = fok && (n0 + IW * u + 8 * s4 + i < N);
                 float t = 0.f;
                 z_and_obj<FBC>(xx[i], yy[i], 0.f, beta, zn[i], zd[i], t, pc);
                 zn[i] = ok ? zn[i] : 0.f;
@@ -491,7 +529,7 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
         // the next block's A operand as soon as the Vt tiles of this block have retired (the
         // side products of this block are still running)
         if (bi + 1 < nb) {
-          mbar_wait(bar_opfree, bi & 1);
+          W3(mbar_wait(bar_opfree, bi & 1), 0);
           tc_fence_after();
           write_op(h);
           __syncwarp();
@@ -499,7 +537,7 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
           load_rows(bi + 2);
         }
         // the slice's partial sums of the block: AccH -> hpart[slice][n][num KP | den KP]
-        mbar_wait(bar_acc, bi & 1);
+        W3(mbar_wait(bar_acc, bi & 1), 1);
         tc_fence_after();
         float* dst = hpart + (size_t(blockIdx.y) * N + n) * (2 * KP);
 #pragma unroll
@@ -524,7 +562,6 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
         }
       } else {
         // publish H~_p of the block: Hn rows (core tiles, hi then lo) and HnT scalars
-        if (bi > 0) mbar_wait(bar_opfree, (bi - 1) & 1);   // W-side products of bi-1 retired
         float lo[KP];
 #pragma unroll
         for (int k = 0; k < KP; ++k) {
@@ -533,6 +570,8 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
           lo[k] = x - hi;
           h[k] = hi;
         }
+        // the split above runs ahead of the wait: the operand buffers are single
+        if (bi > 0) W3(mbar_wait(bar_opfree, (bi - 1) & 1), 0);   // W-side products of bi-1 retired
 #pragma unroll
         for (int g = 0; g < KP / 4; ++g) {
           sts_f128(sb + L::OFF_A + L::core(row, 4 * g), h[4 * g], h[4 * g + 1], h[4 * g + 2], h[4 * g + 3]);
@@ -550,7 +589,7 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
         load_rows(bi + 1);
         if ((bi % FOLD) == FOLD - 1 || bi == nb - 1) {
           // AccW of the last FOLD blocks into the fp64 slab (one owner thread per element)
-          mbar_wait(bar_acc, nfold & 1);
+          W3(mbar_wait(bar_acc, nfold & 1), 1);
           tc_fence_after();
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
@@ -585,12 +624,21 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
         for (int k = 0; k < K; ++k) mypart[size_t(s) * F * K + size_t(row0 + row) * K + k] = 0.0;
     }
   }
+#ifdef BNMF_TC_PROF
+  if (a.prof && lane == 0) {
+    pc_[11] = clock64() - t_start_;
+    long long* dstp = a.prof + ((size_t(blockIdx.y) * gridDim.x + blockIdx.x) * NWARPS3 + warp) * 12;
+#pragma unroll
+    for (int i = 0; i < 12; ++i) dstp[i] = pc_[i];
+  }
+#endif
+#undef W3
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (MODE == MODE_W && threadIdx.x == 0) {
     double t = 0.0;
-    for (int i = 0; i < 2 * TW; ++i) t += s_red[i];
+    for (int i = 0; i < NT * TW; ++i) t += s_red[i];
     a.opart[size_t(blockIdx.y) * gridDim.x + blockIdx.x] = t;
   }
   if (warp == W_VT) tmem_dealloc<512>(tmem);

@@ -53,7 +53,7 @@ struct FusedState {
   long long* prof = nullptr;   // BNMF_TC_PROF=1: wait-cycle counters [grid][48]
   size_t prof_n = 0;
   int cap = 0;                 // BNMF_TC_MAX_CLUSTERS at creation (test knob)
-  bool v1 = true;              // false with BNMF_TC_V2=1 (second-generation kernel, A/B knob)
+  bool v1 = false;             // true with BNMF_TC_V2=0 (first-generation kernel, A/B knob)
   // tcgen05 pass pair over a (column group, 128-row slice) grid: F > 256 or 16 < K <= 32
   bool tc3 = false;
   int t3_gx = 0, t3_r = 0, t3_kp = 16;
@@ -64,12 +64,13 @@ struct FusedState {
   double* kcs = nullptr;       // KKT pass, beta = 1 on the SIMT pair: colsum(W~_p) (K)
 };
 
-// BNMF_TC_V2=1 selects the second-generation kernel (fused_tc2_kernel.cuh: item teams, two
-// issuing warps, a dedicated U team).  It is parity-green but measured slower than the first
-// generation on config 4 (profiles/r02_fused_pass_experiments.md), so v1 stays the default.
+// The single-read pass runs the second-generation kernel (fused_tc2_kernel.cuh: item teams, two
+// issuing warps, a dedicated U team, the H items of the next block ahead of the W items of the
+// current one).  BNMF_TC_V2=0 selects the first-generation kernel (fused_tc_kernel.cuh), kept
+// as the A/B twin (profiles/r02_fused_pass_experiments.md).
 static bool env_tc_v1() {
   const char* c = getenv("BNMF_TC_V2");
-  return !(c && c[0] == '1');
+  return c && c[0] == '0';
 }
 
 // BNMF_TC3=0 keeps the F > 256 / 16 < K <= 32 shapes on the SIMT pair (A/B knob)

@@ -38,17 +38,28 @@ namespace ftc2 {
 using namespace bnmf::tc;
 using namespace bnmf::ftc;
 
-constexpr int NTEAM = 2;
-#ifndef BNMF_TEAM_WARPS
-#define BNMF_TEAM_WARPS 4
+#ifndef BNMF_TC2_NT
+#define BNMF_TC2_NT 2
 #endif
-constexpr int TEAM_WARPS = BNMF_TEAM_WARPS;   // 4 or 8 warps per item team
-constexpr int EPT = 128 / TEAM_WARPS;         // elements of an item per thread (32 or 16)
-constexpr int NCH = EPT / 8;                  // 8-element chunks (one Z k-step each)
+constexpr int NTEAM = BNMF_TC2_NT;            // item teams: 2 (32-wide items) or 4 (16-wide items)
+static_assert(NTEAM == 2 || NTEAM == 4, "2 or 4 item teams");
+#ifndef BNMF_TC2_LOOKAHEAD
+#define BNMF_TC2_LOOKAHEAD 4
+#endif
+// H items of block bi + 1 that run ahead of the W items of block bi (all of them by default):
+// they and the W items of block bi - 1 ... cover the H-update chain of block bi (AccH read-out,
+// DSMEM exchange, ratio, publish), which nothing else can overlap
+constexpr int TC2_LOOKAHEAD = BNMF_TC2_LOOKAHEAD;
+constexpr int TEAM_WARPS = 4;                 // one warp per TMEM lane quadrant
+// TMEM holds 64 Vt columns and 256 Z columns for the items in flight: NTEAM items of IW columns
+constexpr int IW = 64 / NTEAM;                // width of an item: rows (H item) / columns (W item)
+constexpr int EPT = IW;                       // elements of an item per thread
+constexpr int NCH = IW / 8;                   // 8-element chunks (one Z k-step each)
+constexpr int HIT = 32 / IW;                  // H items per V stage
+constexpr int WIT = BN / IW;                  // W items per block
 constexpr int U_WARPS = 4;
 constexpr int W_TMA = 0, W_VT = 1, W_SIDE = 2, W_TEAM0 = 3, W_UTEAM = W_TEAM0 + NTEAM * TEAM_WARPS;
 constexpr int NWARPS2 = W_UTEAM + U_WARPS;    // 23 (15 with 4-warp teams)
-static_assert(TEAM_WARPS == 4 || TEAM_WARPS == 8, "item teams have 4 or 8 warps");
 constexpr int NTHREADS2 = 32 * NWARPS2;         // 480
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
@@ -85,21 +96,21 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* bar_full = bars;           // [NSTAGE] TMA -> teams
   uint64_t* bar_empty = bars + 8;      // [NSTAGE] teams -> TMA
-  uint64_t* bar_dfull = bars + 16;     // [2]
-  uint64_t* bar_dfree = bars + 18;     // [2]
-  uint64_t* bar_zfull = bars + 20;     // [2]
-  uint64_t* bar_zfree = bars + 22;     // [2]
-  uint64_t* bar_hp = bars + 24;        // H~_{p-1} rows of a block in TMEM
-  uint64_t* bar_hpfree = bars + 25;    // the H-side Vt tiles of a block retired
-  uint64_t* bar_hn = bars + 26;        // H~_p of a block in SMEM
-  uint64_t* bar_wdone = bars + 27;     // W-side products of a block retired
-  uint64_t* bar_acch = bars + 28;      // AccH of a block complete
-  uint64_t* bar_accfree = bars + 29;   // AccH read out
-  uint64_t* bar_accw = bars + 30;      // AccW of a fold complete
-  uint64_t* bar_accwfree = bars + 31;  // AccW read out
-  uint64_t* bar_xfull = bars + 32;     // peer's AccH partial landed (tx)
-  uint64_t* bar_xempty = bars + 33;    // peer consumed my partial (remote arrivals)
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 40);
+  uint64_t* bar_dfull = bars + 16;     // [NTEAM]
+  uint64_t* bar_dfree = bars + 20;     // [NTEAM]
+  uint64_t* bar_zfull = bars + 24;     // [NTEAM]
+  uint64_t* bar_zfree = bars + 28;     // [NTEAM]
+  uint64_t* bar_hp = bars + 32;        // H~_{p-1} rows of a block in TMEM
+  uint64_t* bar_hpfree = bars + 33;    // the H-side Vt tiles of a block retired
+  uint64_t* bar_hn = bars + 34;        // H~_p of a block in SMEM
+  uint64_t* bar_wdone = bars + 35;     // W-side products of a block retired
+  uint64_t* bar_acch = bars + 36;      // AccH of a block complete
+  uint64_t* bar_accfree = bars + 37;   // AccH read out
+  uint64_t* bar_accw = bars + 38;      // AccW of a fold complete
+  uint64_t* bar_accwfree = bars + 39;  // AccW read out
+  uint64_t* bar_xfull = bars + 40;     // peer's AccH partial landed (tx)
+  uint64_t* bar_xempty = bars + 41;    // peer consumed my partial (remote arrivals)
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 48);
   __shared__ double s_red[NTEAM * TEAM_WARPS];
   __shared__ float s_nrm[KP], s_cs2[KP];
   __shared__ double s_redu[U_WARPS];
@@ -108,24 +119,24 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
   // optional wait-cycle counters (build with BNMF_TC_PROF=1): lane 0 of every warp
   // accumulates the cycles it spends in each wait category, [CTA][warp][12]
 #ifdef BNMF_TC_PROF
-  long long pc[12];
+  long long pcy_[12];
 #pragma unroll
-  for (int i = 0; i < 12; ++i) pc[i] = 0;
+  for (int i = 0; i < 12; ++i) pcy_[i] = 0;
   const long long t_start = clock64();
 #define PWAIT(bar, parity, cat)                       \
   do {                                                \
     const long long t0_ = clock64();                  \
     mbar_wait(bar, parity);                           \
-    pc[cat] += clock64() - t0_;                       \
+    pcy_[cat] += clock64() - t0_;                       \
   } while (0)
 #define PWAITA(addr, parity, cat)                     \
   do {                                                \
     const long long t0_ = clock64();                  \
     mbar_wait_a(addr, parity);                        \
-    pc[cat] += clock64() - t0_;                       \
+    pcy_[cat] += clock64() - t0_;                       \
   } while (0)
 #define PTIME_BEGIN(v) const long long v = clock64()
-#define PTIME_END(v, cat) pc[cat] += clock64() - v
+#define PTIME_END(v, cat) pcy_[cat] += clock64() - v
 #define PTIME_VAR(v) long long v = 0
 #define PTIME_SET(v) v = clock64()
 #else
@@ -141,6 +152,7 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
   const int row0 = rank ? F0 : 0;
   const int FTr = rank ? F - F0 : (F < F0 ? F : F0);
   const int SH = max(2, (FTr + 31) / 32);
+  const int LA = TC2_LOOKAHEAD < SH ? TC2_LOOKAHEAD : SH;   // H items of block bi + 1 ahead of the W items of bi
   const int npairs = gridDim.x / CL, pi = blockIdx.x / CL;
   const int nblocks = (N + BN - 1) / BN;
   const int nb = pi < nblocks ? (nblocks - 1 - pi) / npairs + 1 : 0;
@@ -156,7 +168,7 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
   const float* C1g = kkt ? Wt : a.C1;
   const float* C2g = kkt ? Wt : a.C2;
   const int den_ones = kkt ? 0 : a.den_ones;
-  const int n_w = kkt ? 0 : SW;   // W items per block
+  const int n_w = kkt ? 0 : WIT;  // W items per block
   const float kappa = float(a.sc.kappa), beta = float(a.sc.beta);
   auto col0 = [&](int blk) { return (pi + blk * npairs) * BN; };
 
@@ -166,7 +178,7 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
       mbar_init(&bar_full[s], 1);
       mbar_init(&bar_empty[s], NTEAM * TEAM_WARPS);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NTEAM; ++b) {
       mbar_init(&bar_dfull[b], 1);
       mbar_init(&bar_dfree[b], TEAM_WARPS);
       mbar_init(&bar_zfull[b], TEAM_WARPS);
@@ -214,41 +226,59 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
 
   if (warp == W_TMA) {
     // ======================= TMA producer ===================================
+    // The ring follows the item sequence: an H item takes one stage (its 32 rows), the W items
+    // of a block take SH stages (all rows of the CTA).  The rows of a block are therefore
+    // loaded twice, the second time from L2.
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int j = 0; j < SH && nb > 0; ++j) tma_prefetch_l2_2d(&mapV, col0(0), row0 + 32 * j);
+      auto load = [&](int blk, int j) {
+        PWAIT(&bar_empty[s], ph ^ 1u, 0);
+        mbar_expect_tx(&bar_full[s], STAGE_BYTES);
+        tma_load_2d(smem + OFF_STAGE + s * STAGE_BYTES, &mapV, &bar_full[s], col0(blk), row0 + 32 * j);
+        if (++s == NSTAGE) { s = 0; ph ^= 1u; }
+      };
+      auto prefetch = [&](int blk) {
+        if (blk < nb)
+          for (int j = 0; j < SH; ++j) tma_prefetch_l2_2d(&mapV, col0(blk), row0 + 32 * j);
+      };
+      prefetch(0);
+      prefetch(1);
       for (int bi = 0; bi < nb; ++bi) {
-        const int n0 = col0(bi);
-        for (int j = 0; j < SH; ++j) {
-          if (bi + 1 < nb) tma_prefetch_l2_2d(&mapV, col0(bi + 1), row0 + 32 * j);
-          PWAIT(&bar_empty[s], ph ^ 1u, 0);
-          mbar_expect_tx(&bar_full[s], STAGE_BYTES);
-          tma_load_2d(smem + OFF_STAGE + s * STAGE_BYTES, &mapV, &bar_full[s], n0, row0 + 32 * j);
-          if (++s == NSTAGE) { s = 0; ph ^= 1u; }
+        prefetch(bi + 2);
+        if (do_h) {
+          const int j0 = (bi == 0 || kkt) ? 0 : LA;
+          const int n_own = SH - j0, n_all = n_own + ((bi + 1 < nb && !kkt) ? LA : 0);
+          for (int t = 0; t < n_all; ++t) {
+            const bool own = t < n_own;
+            load(own ? bi : bi + 1, own ? j0 + t : t - n_own);
+          }
         }
+        if (n_w)
+          for (int j = 0; j < SH; ++j) load(bi, j);
       }
     }
   } else if (warp == W_VT) {
     // ======================= Vt issuer =======================================
-    const uint32_t id32 = idesc_tf32(128, 32, 0, 0);
+    const uint32_t id_vt = idesc_tf32(128, IW, 0, 0);
     const uint64_t d_wa = sdesc(sb + OFF_WA, 128, 512);
     const uint64_t d_hn = sdesc(sb + OFF_HN, 128, 512);
     int c = 0;
     // Vt tile of the next item in sequence: waits until its team has read the previous tile of
-    // the buffer, issues 6 MMAs, commits to dfull
-    auto vt = [&](bool hside, int idx, bool last_h) {
-      const int b = c & 1, m = c >> 1;
+    // the buffer, issues 6 MMAs, commits to dfull.  it = item within the block: B rows IW it..
+    auto vt = [&](bool hside, int it, bool last_h) {
+      const int b = c & (NTEAM - 1), m = c / NTEAM;
       ++c;
       if (m > 0) PWAIT(&bar_dfree[b], (m - 1) & 1, 2);
       tc_fence_after();
       if (elect_one()) {
+        const uint32_t off = uint32_t(it) * (IW / 8) * 512;
         if (hside) {
-          issue_vt(tmem + TM_D + 32 * b, tmem + TM_HP, tmem + TM_HP + 16, dplus(d_wa, idx * 2048),
-                   dplus(d_wa, idx * 2048 + HILO), id32);
+          issue_vt(tmem + TM_D + IW * b, tmem + TM_HP, tmem + TM_HP + 16, dplus(d_wa, off),
+                   dplus(d_wa, off + HILO), id_vt);
         } else {
-          issue_vt(tmem + TM_D + 32 * b, tmem + TM_WT, tmem + TM_WT + 16, dplus(d_hn, idx * 2048),
-                   dplus(d_hn, idx * 2048 + HILO), id32);
+          issue_vt(tmem + TM_D + IW * b, tmem + TM_WT, tmem + TM_WT + 16, dplus(d_hn, off),
+                   dplus(d_hn, off + HILO), id_vt);
         }
         mma_commit(&bar_dfull[b]);
         if (last_h) mma_commit(bar_hpfree);
@@ -257,13 +287,13 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
     };
     for (int bi = 0; bi < nb; ++bi) {
       if (do_h) {
-        const int j0 = (bi == 0 || kkt) ? 0 : 2;
-        const int n_own = SH - j0, n_all = n_own + ((bi + 1 < nb && !kkt) ? 2 : 0);
+        const int j0 = (bi == 0 || kkt) ? 0 : LA;
+        const int n_own = SH - j0, n_all = n_own + ((bi + 1 < nb && !kkt) ? LA : 0);
         for (int t = 0; t < n_all; ++t) {
           const bool own = t < n_own;
           const int j = own ? j0 + t : t - n_own;
           if (j == 0) PWAIT(bar_hp, (own ? bi : bi + 1) & 1, 0);
-          vt(true, j, j == SH - 1);
+          for (int h = 0; h < HIT; ++h) vt(true, j * HIT + h, j == SH - 1 && h == HIT - 1);
         }
       }
       if (n_w) PWAIT(bar_hn, bi & 1, 1);
@@ -276,48 +306,56 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
     const uint64_t d_c1 = sdesc(sb + OFF_C1, 128, 4096);
     const uint64_t d_c2 = sdesc(sb + OFF_C2, 128, 4096);
     const uint64_t d_hnt = sdesc(sb + OFF_HNT, HNT_LBO, HNT_SBO);
+    // acc[:, 0:32] (+)= Z_hi [B_hi | B_lo], acc[:, 0:16] += Z_lo B_hi over the item's NCH k-steps
+    auto side = [&](uint32_t acc, uint32_t z, uint64_t bdesc, uint32_t kstride, bool fresh) {
+#pragma unroll
+      for (int s = 0; s < NCH; ++s) {
+        mma_ts(acc, z + 32 * s, dplus(bdesc, kstride * s), id32, (fresh && s == 0) ? 0u : 1u);
+        mma_ts(acc, z + 32 * s + 8, dplus(bdesc, kstride * s), id16, 1u);
+      }
+    };
     int c = 0;
-    auto side_h = [&](int blk, int idx) {
-      const int b = c & 1, m = c >> 1;
+    // it = H item within the block (IW rows each)
+    auto side_h = [&](int blk, int it) {
+      const int b = c & (NTEAM - 1), m = c / NTEAM;
       ++c;
-      const uint32_t zb = tmem + TM_Z + 128 * b;
+      const uint32_t zb = tmem + TM_Z + 4 * IW * b;
       PWAIT(&bar_zfull[b], m & 1, 0);
-      if (idx == 0 && blk > 0) PWAIT(bar_accfree, (blk - 1) & 1, 1);
+      if (it == 0 && blk > 0) PWAIT(bar_accfree, (blk - 1) & 1, 1);
       tc_fence_after();
       if (elect_one()) {
-        issue_side<256>(tmem + TM_ACCH, zb, dplus(d_c1, idx * 1024), id32, id16, idx == 0);
-        if (!den_ones)
-          issue_side<256>(tmem + TM_ACCH + 32, zb + 16, dplus(d_c2, idx * 1024), id32, id16,
-                          idx == 0);
+        side(tmem + TM_ACCH, zb, dplus(d_c1, it * IW * 32), 256, it == 0);
+        if (!den_ones) side(tmem + TM_ACCH + 32, zb + 16, dplus(d_c2, it * IW * 32), 256, it == 0);
         mma_commit(&bar_zfree[b]);
-        if (idx == SH - 1) mma_commit(bar_acch);
+        if (it == SH * HIT - 1) mma_commit(bar_acch);
       }
       __syncwarp();
     };
     for (int bi = 0; bi < nb; ++bi) {
       if (do_h) {
-        const int j0 = (bi == 0 || kkt) ? 0 : 2;
-        const int n_own = SH - j0, n_all = n_own + ((bi + 1 < nb && !kkt) ? 2 : 0);
+        const int j0 = (bi == 0 || kkt) ? 0 : LA;
+        const int n_own = SH - j0, n_all = n_own + ((bi + 1 < nb && !kkt) ? LA : 0);
         for (int t = 0; t < n_all; ++t) {
           const bool own = t < n_own;
-          side_h(own ? bi : bi + 1, own ? j0 + t : t - n_own);
+          const int j = own ? j0 + t : t - n_own;
+          for (int h = 0; h < HIT; ++h) side_h(own ? bi : bi + 1, j * HIT + h);
         }
       }
       const bool fold_end = (bi % FOLD) == FOLD - 1 || bi == nb - 1;
       for (int u = 0; u < n_w; ++u) {
-        const int b = c & 1, m = c >> 1;
+        const int b = c & (NTEAM - 1), m = c / NTEAM;
         ++c;
-        const uint32_t zb = tmem + TM_Z + 128 * b;
+        const uint32_t zb = tmem + TM_Z + 4 * IW * b;
         const bool fresh = (bi % FOLD) == 0 && u == 0;
         PWAIT(&bar_zfull[b], m & 1, 0);
         if (fresh && bi > 0) PWAIT(bar_accwfree, ((bi / FOLD) - 1) & 1, 2);
         tc_fence_after();
         if (elect_one()) {
-          const uint64_t bh = dplus(d_hnt, u * 8 * HNT_LBO);
-          issue_side<2 * HNT_LBO>(tmem + TM_ACCW, zb, bh, id32, id16, fresh);
-          issue_side<2 * HNT_LBO>(tmem + TM_ACCW + 32, zb + 16, bh, id32, id16, fresh);
+          const uint64_t bh = dplus(d_hnt, u * (IW / 4) * HNT_LBO);
+          side(tmem + TM_ACCW, zb, bh, 2 * HNT_LBO, fresh);
+          side(tmem + TM_ACCW + 32, zb + 16, bh, 2 * HNT_LBO, fresh);
           mma_commit(&bar_zfree[b]);
-          if (u == SW - 1) {
+          if (u == WIT - 1) {
             mma_commit(bar_wdone);
             if (fold_end) mma_commit(bar_accw);
           }
@@ -328,12 +366,11 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
   } else if (warp < W_UTEAM) {
     // ======================= item teams ======================================
     const int team = (warp - W_TEAM0) / TEAM_WARPS;
-    const int c0 = (((warp - W_TEAM0) % TEAM_WARPS) >> 2) * EPT;   // this warp's columns of an item
     const int q = warp & 3;          // TMEM lane quadrant
     const int row = 32 * q + lane;   // TMEM lane: n (H items) or f - row0 (W items)
     const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16);
-    const uint32_t dcol = lane_base + TM_D + 32 * team + c0;
-    const uint32_t zcol = lane_base + TM_Z + 128 * team + 4 * c0;
+    const uint32_t dcol = lane_base + TM_D + IW * team;
+    const uint32_t zcol = lane_base + TM_Z + 4 * IW * team;
     const uint32_t dfull_a = smem_u32(&bar_dfull[team]), dfree_a = smem_u32(&bar_dfree[team]);
     const uint32_t zfull_a = smem_u32(&bar_zfull[team]), zfree_a = smem_u32(&bar_zfree[team]);
     const uint32_t full_a = smem_u32(bar_full), empty_a = smem_u32(bar_empty);
@@ -371,16 +408,17 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
       ++m;
     };
 
-    // ---------------- H item: rows row0 + 32 idx + [0, 32) of column n0 + row ----------------
-    auto h_item = [&](int n0, int idx, int s, uint32_t ph) {
+    // ---------------- H item: rows row0 + IW it + [0, IW) of column n0 + row (stage s) -------
+    auto h_item = [&](int n0, int it, int s, uint32_t ph) {
       PTIME_BEGIN(t_it);
       float x[EPT], y[EPT];
       PWAITA(full_a + 8 * s, ph, 2);
-      const uint32_t xa = sb + OFF_STAGE + s * STAGE_BYTES + c0 * VROWB + row * 4;
+      const int r0 = IW * it;
+      const uint32_t xa = sb + OFF_STAGE + s * STAGE_BYTES + (r0 & 31) * VROWB + row * 4;
 #pragma unroll
       for (int i = 0; i < EPT; ++i) x[i] = lds_f32(xa + i * VROWB);
       take_tile(y, 0);
-      const bool full = n0 + BN <= N && (rows_full || 32 * idx + 32 <= FTr);
+      const bool full = n0 + BN <= N && (rows_full || r0 + IW <= FTr);
       const bool nok = n0 + row < N;
 #pragma unroll
       for (int s4 = 0; s4 < NCH; ++s4) {
@@ -393,7 +431,7 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
         if (!full) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const bool ok = nok && (32 * idx + c0 + 8 * s4 + i < FTr);
+            const bool ok = nok && (r0 + 8 * s4 + i < FTr);
             zn[i] = ok ? zn[i] : 0.f;
             zd[i] = ok ? zd[i] : 0.f;
           }
@@ -405,14 +443,14 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
       PTIME_END(t_it, 5);
     };
 
-    // ---------------- W item: row row0 + row, columns n0 + 32 idx + [0, 32) ------------------
+    // ---------------- W item: row row0 + row, columns n0 + IW idx + [0, IW) ------------------
     auto w_item = [&](int n0, int idx, uint32_t xrow) {
       PTIME_BEGIN(t_it);
       float x[EPT], y[EPT];
       if (q < SH) {
 #pragma unroll
         for (int i = 0; i < EPT; i += 4) {
-          const float4 v = lds_f128(xrow + 128 * idx + 4 * (c0 + i));
+          const float4 v = lds_f128(xrow + 4 * IW * idx + 4 * i);
           x[i] = v.x; x[i + 1] = v.y; x[i + 2] = v.z; x[i + 3] = v.w;
         }
       } else {
@@ -459,7 +497,7 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
             float o0 = 0.f;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              const bool ok = fok && (n0 + 32 * idx + c0 + 8 * s4 + i < N);
+              const bool ok = fok && (n0 + IW * idx + 8 * s4 + i < N);
               float t = 0.f;
               z_and_obj<FBC>(xx[i], yy[i], 0.f, beta, zn[i], zd[i], t, pc);
               zn[i] = ok ? zn[i] : 0.f;
@@ -477,57 +515,54 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
       PTIME_END(t_it, 6);
     };
 
-    int c = 0;                 // item sequence number
-    int s_cur = 0, s_nxt = 0;  // stage slot of rows 0.. of block bi / bi + 1
-    uint32_t p_cur = 0, p_nxt = 0;
-    auto slot_of = [&](int s0, uint32_t p0, int j, uint32_t& ph) {
-      int s = s0 + j;
-      ph = p0;
-      if (s >= NSTAGE) { s -= NSTAGE; ph ^= 1u; }
-      return s;
-    };
+    int c = 0;                 // sequence number of the next item
+    int sl = 0;                // ring slot of the next stage in load order
+    uint32_t sp = 0;           // and its phase
     for (int bi = 0; bi < nb; ++bi) {
-      s_nxt = s_cur + SH;
-      p_nxt = p_cur;
-      if (s_nxt >= NSTAGE) { s_nxt -= NSTAGE; p_nxt ^= 1u; }
       if (do_h) {
-        const int j0 = (bi == 0 || kkt) ? 0 : 2;
-        const int n_own = SH - j0, n_all = n_own + ((bi + 1 < nb && !kkt) ? 2 : 0);
-        for (int t = 0; t < n_all; ++t) {
-          const bool mine = (c & 1) == team;
-          ++c;
-          if (mine) {
-            const bool own = t < n_own;
-            const int j = own ? j0 + t : t - n_own;
-            uint32_t ph;
-            const int s = slot_of(own ? s_cur : s_nxt, own ? p_cur : p_nxt, j, ph);
-            h_item(col0(own ? bi : bi + 1), j, s, ph);
+        const int j0 = (bi == 0 || kkt) ? 0 : LA;
+        const int n_own = SH - j0, n_all = n_own + ((bi + 1 < nb && !kkt) ? LA : 0);
+        // the team's items of the list: item i of the list has sequence number c + i
+        for (int i = (team - c) & (NTEAM - 1); i < n_all * HIT; i += NTEAM) {
+          const int t = i / HIT;
+          const bool own = t < n_own;
+          const int j = own ? j0 + t : t - n_own;
+          int s = sl + t;
+          uint32_t ph = sp;
+          if (s >= NSTAGE) { s -= NSTAGE; ph ^= 1u; }
+          h_item(col0(own ? bi : bi + 1), j * HIT + (i - t * HIT), s, ph);
+          // the stage goes back after the item's Z store (its x values are consumed); only
+          // HIT of the NTEAM teams touch a stage, each arrives for NTEAM / HIT
+          if (lane == 0) mbar_arrive_cnt_a(empty_a + 8 * s, NTEAM / HIT);
+        }
+        c += n_all * HIT;
+        sl += n_all;
+        if (sl >= NSTAGE) { sl -= NSTAGE; sp ^= 1u; }
+      }
+      if (n_w) {
+        // this warp's V rows of the block are stage q of the block's SH stages
+        uint32_t xrow = 0;
+        if (q < SH) {
+          int s = sl + q;
+          uint32_t ph = sp;
+          if (s >= NSTAGE) { s -= NSTAGE; ph ^= 1u; }
+          PWAITA(full_a + 8 * s, ph, 3);
+          xrow = sb + OFF_STAGE + s * STAGE_BYTES + lane * VROWB;
+        }
+        const int n0 = col0(bi);
+        for (int u = (team - c) & (NTEAM - 1); u < n_w; u += NTEAM) w_item(n0, u, xrow);
+        c += n_w;
+        // every team hands the V stages of the block back
+        if (lane == 0) {
+          for (int j = 0; j < SH; ++j) {
+            int s = sl + j;
+            if (s >= NSTAGE) s -= NSTAGE;
+            mbar_arrive_a(empty_a + 8 * s);
           }
         }
+        sl += SH;
+        if (sl >= NSTAGE) { sl -= NSTAGE; sp ^= 1u; }
       }
-      // this warp's V rows of the block are stage q
-      uint32_t xrow = 0;
-      if (q < SH && n_w) {
-        uint32_t ph;
-        const int s = slot_of(s_cur, p_cur, q, ph);
-        PWAITA(full_a + 8 * s, ph, 3);
-        xrow = sb + OFF_STAGE + s * STAGE_BYTES + lane * VROWB;
-      }
-      const int n0 = col0(bi);
-      for (int u = 0; u < n_w; ++u) {
-        const bool mine = (c & 1) == team;
-        ++c;
-        if (mine) w_item(n0, u, xrow);
-      }
-      // both teams hand the V stages of the block back
-      if (lane == 0) {
-        for (int j = 0; j < SH; ++j) {
-          uint32_t ph;
-          mbar_arrive_a(empty_a + 8 * slot_of(s_cur, p_cur, j, ph));
-        }
-      }
-      s_cur = s_nxt;
-      p_cur = p_nxt;
     }
     for (int o = 16; o > 0; o >>= 1) obj += __shfl_down_sync(0xffffffffu, obj, o);
     if (lane == 0) s_red[warp - W_TEAM0] = obj;
@@ -596,17 +631,48 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
     else tc_fence_before();
     int nfold = 0;
     double kres = 0.0;
+    bool fold_pending = false;
+    // add the TMEM W sums of the last FOLD blocks into the fp64 slab; one owner thread per
+    // slab element: the first fold stores, later folds are fire-and-forget fp64 reductions
+    // applied in program order
+    auto fold = [&]() {
+      PWAIT(bar_accw, nfold & 1, 5);
+      tc_fence_after();
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        float v[32];
+        tmem_ld32(lane_base + TM_ACCW + 32 * s, v);
+        if (s == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_accwfree);
+        }
+        if (row < FTr) {
+          double* dst = mypart + size_t(s) * F * K + size_t(row0 + row) * K;
+#pragma unroll
+          for (int k = 0; k < KP; ++k) {
+            if (k < K) {
+              const double add = double(v[k]) + double(v[KP + k]);
+              if (nfold == 0) dst[k] = add;
+              else atomicAdd(dst + k, add);
+            }
+          }
+        }
+      }
+      ++nfold;
+    };
     for (int bi = 0; bi < nb; ++bi) {
       const int n = col0(bi) + row;
       float hv[KP];
       PTIME_VAR(t_chain);
+      // H~_{p-1} of the next block: its H items run before the H update of bi
+      if (do_h && bi + 1 < nb) {
+        PWAIT(bar_hpfree, bi & 1, 0);
+        tc_fence_after();
+        write_hp(h1);
+      }
+      if (fold_pending) fold();
       if (do_h) {
-        // H~_{p-1} of the next block: its first H items run before the H update of bi
-        if (bi + 1 < nb) {
-          PWAIT(bar_hpfree, bi & 1, 0);
-          tc_fence_after();
-          write_hp(h1);
-        }
         // U1: AccH of the block read out (and sent to the peer CTA)
         float unum[KP], uden[KP];
         PWAIT(bar_acch, bi & 1, 1);
@@ -759,36 +825,12 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
 #pragma unroll
       for (int k = 0; k < KP; ++k) h0[k] = h1[k];
       load_rows(bi + 2, h1);
-      if ((bi % FOLD) == FOLD - 1 || bi == nb - 1) {
-        // add the TMEM W sums of the last FOLD blocks into the fp64 slab; one
-        // owner thread per slab element: the first fold stores, later folds are
-        // fire-and-forget fp64 reductions applied in program order
-        PWAIT(bar_accw, nfold & 1, 5);
-        tc_fence_after();
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          float v[32];
-          tmem_ld32(lane_base + TM_ACCW + 32 * s, v);
-          if (s == 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar_accwfree);
-          }
-          if (row < FTr) {
-            double* dst = mypart + size_t(s) * F * K + size_t(row0 + row) * K;
-#pragma unroll
-            for (int k = 0; k < KP; ++k) {
-              if (k < K) {
-                const double add = double(v[k]) + double(v[KP + k]);
-                if (nfold == 0) dst[k] = add;
-                else atomicAdd(dst + k, add);
-              }
-            }
-          }
-        }
-        ++nfold;
-      }
+      // the fold of a finished group waits for the W products of this block, which now run
+      // after the H items of the next one: it is taken at the top of the next iteration so
+      // that it does not hold back H~_{p-1} of the block after next
+      fold_pending = !kkt && ((bi % FOLD) == FOLD - 1 || bi == nb - 1);
     }
+    if (fold_pending) fold();
     if (kkt) {
       for (int o = 16; o > 0; o >>= 1) kres += __shfl_down_sync(0xffffffffu, kres, o);
       if (lane == 0) s_redu[warp - W_UTEAM] = kres;
@@ -799,10 +841,10 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
   }
 #ifdef BNMF_TC_PROF
   if (a.prof && lane == 0) {
-    pc[11] = clock64() - t_start;
+    pcy_[11] = clock64() - t_start;
     long long* dst = a.prof + (size_t(blockIdx.x) * NWARPS2 + warp) * 12;
 #pragma unroll
-    for (int i = 0; i < 12; ++i) dst[i] = pc[i];
+    for (int i = 0; i < 12; ++i) dst[i] = pcy_[i];
   }
 #endif
 #undef PWAIT

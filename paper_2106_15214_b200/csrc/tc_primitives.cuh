@@ -83,6 +83,9 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
 __device__ __forceinline__ void mbar_arrive_a(uint32_t a) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_cnt_a(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
 
 // ---- TMA ------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch(const void* tmap) {

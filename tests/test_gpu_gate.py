@@ -34,7 +34,7 @@ CASES = {
 }
 
 
-def _run_case(name, cap=None, expect_tc=None, v2=False):
+def _run_case(name, cap=None, expect_tc=None, v1=False):
     z = load_golden("gate.npz")
     gen, K, beta, kappa = CASES[name]
     v = gen().astype(np.float32)
@@ -44,8 +44,8 @@ def _run_case(name, cap=None, expect_tc=None, v2=False):
     old = os.environ.get("BNMF_TC_MAX_CLUSTERS")
     if cap is not None:
         os.environ["BNMF_TC_MAX_CLUSTERS"] = str(cap)
-    if v2:
-        os.environ["BNMF_TC_V2"] = "1"     # the experimental second-generation kernel
+    if v1:
+        os.environ["BNMF_TC_V2"] = "0"     # the first-generation kernel (A/B twin)
     try:
         for algo in ("jmm", "bmm"):
             ref = z[f"{name}_{algo}/obj"]
@@ -72,7 +72,7 @@ def _run_case(name, cap=None, expect_tc=None, v2=False):
             err = np.linalg.norm(res.factors.w - wref) / np.linalg.norm(wref)
             assert err <= 2e-2, (name, algo, cap, err)
     finally:
-        if v2:
+        if v1:
             del os.environ["BNMF_TC_V2"]
         if cap is not None:
             if old is None:
@@ -93,10 +93,10 @@ def test_config4_steady_state_schedule_200_iterations(name, cap):
 
 
 @pytest.mark.parametrize("name,cap", [("cfg4s", 2), ("cfg4b", None), ("cfg4k", 1)])
-def test_second_generation_kernel_200_iterations(name, cap):
-    """BNMF_TC_V2=1 (fused_tc2_kernel.cuh: item teams, two issuing warps, U team) holds the
-    same gate; it is opt-in because it measured slower (profiles/r02_fused_pass_experiments.md)."""
-    _run_case(name, cap=cap, expect_tc=True, v2=True)
+def test_first_generation_kernel_200_iterations(name, cap):
+    """BNMF_TC_V2=0 (fused_tc_kernel.cuh: 16 epilogue warps in lock-step, one issuing warp), the
+    A/B twin of the default second-generation kernel, holds the same gate."""
+    _run_case(name, cap=cap, expect_tc=True, v1=True)
 
 
 @pytest.mark.parametrize("name", ["cfg4s", "cfg4b", "cfg4k", "cfg2", "cfg3"])

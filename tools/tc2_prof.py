@@ -21,14 +21,16 @@ kind, grid, cl, f0 = ctx.pass_info()
 lib = _native.load()
 buf = (ctypes.c_longlong * (grid * 288))()
 n = lib.bnmf_tc_prof_read(buf, grid * 288)
-NW = int(os.environ.get('BNMF_TEAM_WARPS', '8')) * 2 + 7
+NT = int(os.environ.get('BNMF_TC2_NT', '4'))
+NW = 4 * NT + 7
 a = np.array(buf[:grid * 12 * NW], dtype=np.int64).reshape(grid, NW, 12)
 roles = {
     0: ("TMA", {0: "empty"}),
     1: ("Vt issuer", {0: "hp", 1: "hn", 2: "dfree"}),
     2: ("side issuer", {0: "zfull", 1: "accfree", 2: "accwfree"}),
     3: ("team0 q3", {0: "dfull(H)", 1: "dfull(W)", 2: "full(H)", 3: "full(W)", 4: "zfree", 5: "H items", 6: "W items"}),
-    3 + (NW - 7) // 2: ("team1 q3", {0: "dfull(H)", 1: "dfull(W)", 2: "full(H)", 3: "full(W)", 4: "zfree", 5: "H items", 6: "W items"}),
+    7: ("team1 q3", {0: "dfull(H)", 1: "dfull(W)", 2: "full(H)", 3: "full(W)", 4: "zfree", 5: "H items", 6: "W items"}),
+    4 * NT - 1: ("last team q3", {0: "dfull(H)", 1: "dfull(W)", 2: "full(H)", 3: "full(W)", 4: "zfree", 5: "H items", 6: "W items"}),
     NW - 4: ("U team q3", {0: "hpfree", 1: "acch", 2: "xempty", 3: "xfull", 4: "wdone", 5: "accw", 6: "  acch->sends issued", 7: "acch->hn chain (incl. xempty/xfull/wdone waits)", 8: "  acch->AccH read", 9: "  acch->ratio done", 10: "  acch->peer partial added"}),
 }
 print(f"grid {grid}, N {N}")

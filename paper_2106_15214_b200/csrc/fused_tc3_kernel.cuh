@@ -332,10 +332,10 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
     for (int bi = 0; bi < nb; ++bi) {
       const int n0 = col0(bi);
       if (MODE == MODE_H) {
-        for (int it = 0; it < SH * HIT; ++it) {
-          const bool mine = (c & (NT - 1)) == team;
-          ++c;
-          if (!mine) continue;
+        // the team's items of the block: item it has sequence number c + it
+        const int it0 = (team - c) & (NT - 1);
+        c += SH * HIT;
+        for (int it = it0; it < SH * HIT; it += NT) {
           // ---------- H item: rows row0 + r0 + [0, IW) of column n0 + row ----------
           const int j = it / HIT, r0 = IW * it;
           uint32_t ph;
@@ -388,10 +388,9 @@ pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restric
           W3(mbar_wait_a(full_a + 8 * s, ph), 2);
           xrow = sb + s * STAGE_BYTES + lane * VROWB;
         }
-        for (int u = 0; u < WIT; ++u) {
-          const bool mine = (c & (NT - 1)) == team;
-          ++c;
-          if (!mine) continue;
+        const int u0 = (team - c) & (NT - 1);
+        c += WIT;
+        for (int u = u0; u < WIT; u += NT) {
           // ---------- W item: row row0 + row, columns n0 + IW u + [0, IW) ----------
           float x[IW], y[IW];
           if (q < SH) {

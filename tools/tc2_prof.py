@@ -14,7 +14,8 @@ ctx = solver.get_context(0, "fp32")
 ctx.set_dense(v, 0.0)
 ctx.set_factors(w0, h0)
 cfg = bn.SolverConfig(beta=1.5, rank=12, algorithm="jmm", tol=1e-300, kappa=0.0, max_outer_iters=2)
-ctx.begin(solver.make_params(cfg, 0.0, kkt=False), 2)
+KKT = os.environ.get('KKT', '0') == '1'   # KKT=1: the counters of the H-side KKT pass (the last launch)
+ctx.begin(solver.make_params(cfg, 0.0, kkt=KKT), 2)
 ctx.step_timed(2)
 ctx.sync()
 kind, grid, cl, f0 = ctx.pass_info()

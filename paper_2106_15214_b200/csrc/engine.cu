@@ -530,7 +530,17 @@ struct Engine : EngineBase {
   }
 
   int colsums(const T* M, int slot) {
-    col_sums<T><<<(K + 31) / 32, 32, 0, stream>>>(M, F, K, colsum, st, slot);
+    // K <= 128 (the engine's rank cap) < CS_THREADS
+    const size_t row_bytes = size_t(K) * sizeof(T);
+    const int rows = int(std::max<size_t>(1, std::min<size_t>(size_t(F), CS_SMEM_MAX / row_bytes)));
+    const size_t smem = size_t(rows) * row_bytes;
+    static bool attr_set = false;
+    if (!attr_set) {
+      CK(cudaFuncSetAttribute(col_sums<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              int(CS_SMEM_MAX)));
+      attr_set = true;
+    }
+    col_sums<T><<<1, CS_THREADS, smem, stream>>>(M, F, K, colsum, rows, st, slot);
     CK(cudaGetLastError());
     launches += 1;
     return 0;

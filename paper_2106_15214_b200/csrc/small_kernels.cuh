@@ -70,24 +70,42 @@ __global__ void update_w(const T* __restrict__ base, const double* __restrict__ 
 // Column sums of an F x K matrix -> double K-vector, one thread per column, rows added in
 // order: the order of numpy's sum over axis 0, so that the beta = 1 denominators (and the
 // exact-equality stop rule that can hang on their last bit) match the reference bit for bit.
-// Sixteen rows are loaded before any is added (the loads, not the adds, are the latency).
+// The loads, not the adds, are the latency (F dependent round trips to L2 took 36 us at
+// config 1), so one block streams the matrix through shared memory with cp.async, as many
+// rows per round as fit, and thread k then adds its column from there.
+constexpr int CS_THREADS = 256;
+constexpr size_t CS_SMEM_MAX = 160 * 1024;
+
 template <typename T>
-__global__ void col_sums(const T* __restrict__ M, int F, int K, double* __restrict__ out,
-                         const RunState* st, int slot) {
+__global__ void __launch_bounds__(CS_THREADS)
+col_sums(const T* __restrict__ M, int F, int K, double* __restrict__ out, int rows_per_round,
+         const RunState* st, int slot) {
   if (st && !iter_active(st, slot)) return;
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= K) return;
-  double s = 0.0;
-  int f = 0;
-  for (; f + 16 <= F; f += 16) {
-    T v[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) v[u] = M[(size_t)(f + u) * K + k];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) s += double(v[u]);
+  extern __shared__ __align__(16) unsigned char cs_smem[];
+  T* buf = reinterpret_cast<T*>(cs_smem);
+  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(buf));
+  double s[(128 + CS_THREADS - 1) / CS_THREADS] = {0.0};   // K <= 128: one column per thread
+  for (int f0 = 0; f0 < F; f0 += rows_per_round) {
+    const int rows = min(rows_per_round, F - f0);
+    const int n = rows * K;
+    const T* src = M + (size_t)f0 * K;
+    for (int i = threadIdx.x; i < n; i += CS_THREADS) {
+      if (sizeof(T) == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sbase + 8u * i), "l"(src + i)
+                     : "memory");
+      else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sbase + 4u * i), "l"(src + i)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < K) {
+      const int k = threadIdx.x;
+      for (int r = 0; r < rows; ++r) s[0] += double(buf[r * K + k]);
+    }
+    __syncthreads();
   }
-  for (; f < F; ++f) s += double(M[(size_t)f * K + k]);
-  out[k] = s;
+  if (threadIdx.x < K) out[threadIdx.x] = s[0];
 }
 
 // norms[k] = sqrt(sum_f W[f,k]^2); Wn = W / norms (solver.py:167-171).

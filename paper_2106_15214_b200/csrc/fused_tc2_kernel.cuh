@@ -3,7 +3,7 @@
 // arithmetic as fused_tc_kernel.cuh (the v1 kernel; read its header first);
 // what changes is who does what:
 //
-//   warp 0        TMA producer (V stages, L2 prefetch of the next block)
+//   warp 0        TMA producer (V stages in item order, L2 prefetch two blocks ahead)
 //   warp 1        Vt issuer: the W~H~ tiles of every item (3xTF32), TMEM owner
 //   warp 2        side issuer: the W-side / H-side products of every item
 //   warps 3..6    item team 0: items with an even sequence number
@@ -28,6 +28,19 @@
 //   dfree[b]  team -> Vt issuer     tile read into registers
 //   zfull[b]  team -> side issuer   Z stored to TMEM
 //   zfree[b]  side issuer -> team   side products of the item retired (commit)
+//
+// Item order and the V ring.  The H update of block b (AccH read-out, DSMEM
+// exchange with the peer, ratio, publish: ~3000 cycles on the U team) stands
+// between the last H item of b and its first W item, and only H items of later
+// blocks can run beside it.  The items therefore go H(0), H(1), W(0), H(2),
+// W(1), H(3), W(2), ...: all H items of block b+1 ahead of the W items of
+// block b, so that the update of b runs under the W items of b-1.  The 7-stage
+// ring follows that sequence instead of the block structure of V: an H item
+// takes one stage (its 32 rows, released by its team after the Z store), the W
+// items of a block take the block's SH stages (released by both teams after
+// the last W item).  Every V row thus enters shared memory twice, the second
+// time from L2 (the producer prefetches two blocks ahead); DRAM traffic is
+// unchanged.  This is the default single-read kernel; BNMF_TC_V2=0 selects v1.
 #pragma once
 
 #include "fused_tc_kernel.cuh"

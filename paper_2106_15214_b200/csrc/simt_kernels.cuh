@@ -42,9 +42,15 @@ __host__ __device__ inline int kstride(int K) { return (K & 1) ? K : K + 1; }
 template <typename T>
 __device__ __forceinline__ void load_rows(T* dst, const T* __restrict__ src, int rows,
                                           int valid, int K, int ks) {
+  // (r, k) of element i advance with i by (blockDim / K, blockDim % K): two divisions per call
+  // instead of one per element
+  const int dr = blockDim.x / K, dk = blockDim.x - dr * K;
+  int r = threadIdx.x / K, k = threadIdx.x - r * K;
   for (int i = threadIdx.x; i < rows * K; i += blockDim.x) {
-    int r = i / K, k = i - r * K;
-    dst[r * ks + k] = r < valid ? src[(size_t)r * K + k] : T(0);
+    dst[r * ks + k] = r < valid ? src[i] : T(0);
+    r += dr;
+    k += dk;
+    if (k >= K) { k -= K; ++r; }
   }
 }
 
@@ -61,6 +67,16 @@ __device__ __forceinline__ void z_tile(const T* __restrict__ V, size_t ldv, int 
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r = w & 3, cp = w >> 2, g = lane >> 2, t = lane & 3;
     double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    // the V values of the thread's four elements are requested before the product chain, so
+    // that their latency runs under it
+    T xv[2][2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int f = 8 * r + g, n = 8 * (2 * cp + c) + 2 * t + e;
+        xv[c][e] = (f0 + f < F && n0 + n < N) ? V[(size_t)(f0 + f) * ldv + (n0 + n)] : T(0);
+      }
     for (int k0 = 0; k0 < K; k0 += 4) {
       const int k = k0 + t;
       const double a = k < K ? Ws[(8 * r + g) * ks + k] : 0.0;
@@ -78,7 +94,7 @@ __device__ __forceinline__ void z_tile(const T* __restrict__ V, size_t ldv, int 
         T zn = T(0), zd = T(0);
         if (f0 + f < F && n0 + n < N) {
           const T y = acc[c][e] + kappa;
-          const T x = V[(size_t)(f0 + f) * ldv + (n0 + n)];
+          const T x = xv[c][e];
           if (MODE == PM_KKT) {
             zn = grad_core<BC, T>(x, y, beta);
           } else {

@@ -7,11 +7,11 @@ N = 4194304
 v = synthetic.config4(N=N, dtype=np.float32)
 w0, h0 = synthetic.uniform_init(256, N, 12, seed=112)
 vp = torch.from_numpy(v).pin_memory().numpy()
-cfg = bn.SolverConfig(beta=1.5, rank=12, algorithm="jmm", tol=1e-300, kappa=0.0, max_outer_iters=32)
-bn.fit(vp, cfg, init=(w0, h0), dtype="fp32", kkt=False)   # warm
+cfg = bn.SolverConfig(beta=1.5, rank=12, algorithm="jmm", tol=1e-300, kappa=0.0, max_outer_iters=50)
+bn.fit(vp, cfg, init=(w0, h0), dtype="fp32")   # warm
 t = time.perf_counter()
 pr = cProfile.Profile(); pr.enable()
-r = bn.fit(vp, cfg, init=(w0, h0), dtype="fp32", kkt=False)
+r = bn.fit(vp, cfg, init=(w0, h0), dtype="fp32")
 pr.disable()
 print("fit s", time.perf_counter() - t)
 pstats.Stats(pr).sort_stats("cumulative").print_stats(18)

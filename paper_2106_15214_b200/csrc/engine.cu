@@ -423,9 +423,15 @@ struct Engine : EngineBase {
     int ks = kstride(K);
     return size_t(ST_TF * ks + 3 * ST_NC * ks + 2 * ST_TF * (ST_NC + 1)) * sizeof(T);
   }
+  // the fp64 H-side pass double-buffers its row stage when two copies fit
+  int hside_nbuf() const {
+    if (!std::is_same<T, double>::value) return 1;
+    int ks = kstride(K);
+    return size_t(ST_NC * ks + 6 * ST_TF * ks + 2 * ST_TF * (ST_NC + 1)) * sizeof(T) <= 200 * 1024 ? 2 : 1;
+  }
   size_t smem_hside() const {
     int ks = kstride(K);
-    return size_t(ST_NC * ks + 3 * ST_TF * ks + 2 * ST_TF * (ST_NC + 1)) * sizeof(T);
+    return size_t(ST_NC * ks + hside_nbuf() * 3 * ST_TF * ks + 2 * ST_TF * (ST_NC + 1)) * sizeof(T);
   }
   size_t smem_obj() const { return size_t((ST_TF + ST_NC) * kstride(K)) * sizeof(T); }
 
@@ -449,7 +455,7 @@ struct Engine : EngineBase {
     size_t sm = smem_hside();
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
     kern<<<n_hblocks, ST_THREADS, sm, stream>>>(V, ldv, F, N, K, Wp, Hp, C1, C2, Hb, Ho, colsum,
-                                                den_ones, sc, hpart, st, slot);
+                                                den_ones, sc, hpart, hside_nbuf(), st, slot);
     CK(cudaGetLastError());
     launches += 1;
     return 0;

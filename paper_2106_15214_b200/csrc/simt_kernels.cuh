@@ -54,6 +54,26 @@ __device__ __forceinline__ void load_rows(T* dst, const T* __restrict__ src, int
   }
 }
 
+// The same copy with cp.async (8-byte elements): the caller commits the group and waits for it
+// one tile later, so the L2 round trip of a tile's rows runs under the previous tile's work.
+__device__ __forceinline__ void load_rows_async(double* dst, const double* __restrict__ src,
+                                                int rows, int valid, int K, int ks) {
+  const int dr = blockDim.x / K, dk = blockDim.x - dr * K;
+  int r = threadIdx.x / K, k = threadIdx.x - r * K;
+  const unsigned d0 = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  for (int i = threadIdx.x; i < rows * K; i += blockDim.x) {
+    if (r < valid)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d0 + 8u * (r * ks + k)),
+                   "l"(src + i)
+                   : "memory");
+    else
+      dst[r * ks + k] = 0.0;
+    r += dr;
+    k += dk;
+    if (k >= K) { k -= K; ++r; }
+  }
+}
+
 // Z tile for rows [f0, f0+TF) x cols [n0, n0+NC): y = W[f,:] . H[:,n] + kappa,
 // then (zn, zd) by the beta rule (or the KKT gradient core in zn).  Entries
 // outside the matrix are 0 so they never contribute.
@@ -264,15 +284,16 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
            const T* __restrict__ C1w, const T* __restrict__ C2w,
            const T* __restrict__ Hbase, T* __restrict__ Hout,
            const double* __restrict__ colsum_c2, int den_ones, Scalars sc,
-           double* __restrict__ part, const RunState* st, int slot) {
+           double* __restrict__ part, int nbuf, const RunState* st, int slot) {
   if (!iter_active(st, slot)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int ks = kstride(K);
+  // nbuf (1 or 2) copies of the row stage [Ws | C1s | C2s]; two when they fit (fp64 path)
   T* Hs = reinterpret_cast<T*>(smem_raw);
   T* Ws = Hs + ST_NC * ks;
   T* C1s = Ws + ST_TF * ks;
   T* C2s = C1s + ST_TF * ks;
-  T* Zn = C2s + ST_TF * ks;
+  T* Zn = Ws + nbuf * 3 * ST_TF * ks;
   T* Zd = Zn + ST_TF * (ST_NC + 1);
   __shared__ double red[ST_THREADS / 32];
 
@@ -291,18 +312,38 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
 #pragma unroll
     for (int j = 0; j < NJ; ++j) { dn[j][0] = dn[j][1] = 0.0; dd[j][0] = dd[j][1] = 0.0; }
     const bool use_den = (MODE != PM_KKT) && !den_ones;
-    for (int f0 = 0; f0 < F; f0 += ST_TF) {
-      __syncthreads();
-      int valid_f = min(ST_TF, F - f0);
-      load_rows(Ws, Wp + (size_t)f0 * K, ST_TF, valid_f, K, ks);
+    const int bstride = 3 * ST_TF * ks;   // doubles between the two row stages
+    // rows of tile f0 into stage b, one cp.async group
+    auto stage = [&](int f0, int b) {
+      const int valid_f = min(ST_TF, F - f0);
+      load_rows_async(Ws + b * bstride, Wp + (size_t)f0 * K, ST_TF, valid_f, K, ks);
       if (MODE != PM_KKT) {
-        load_rows(C1s, C1w + (size_t)f0 * K, ST_TF, valid_f, K, ks);
-        if (use_den) load_rows(C2s, C2w + (size_t)f0 * K, ST_TF, valid_f, K, ks);
+        load_rows_async(C1s + b * bstride, C1w + (size_t)f0 * K, ST_TF, valid_f, K, ks);
+        if (use_den) load_rows_async(C2s + b * bstride, C2w + (size_t)f0 * K, ST_TF, valid_f, K, ks);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (nbuf == 2) stage(0, 0);
+    int it = 0;
+    for (int f0 = 0; f0 < F; f0 += ST_TF, ++it) {
+      const int b = nbuf == 2 ? (it & 1) : 0;
+      __syncthreads();   // the previous tile's products have read the other stage and Zn / Zd
+      if (nbuf == 2) {
+        const bool more = f0 + ST_TF < F;
+        if (more) stage(f0 + ST_TF, b ^ 1);
+        if (more) asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else asm volatile("cp.async.wait_group 0;" ::: "memory");
+      } else {
+        stage(f0, 0);
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
       __syncthreads();
-      z_tile<BC, MODE, T>(V, ldv, F, N, f0, n0, Ws, Hs, K, ks, kappa, beta, Zn, Zd);
+      const double* Wb = Ws + b * bstride;
+      const double* C1b = C1s + b * bstride;
+      const double* C2b = C2s + b * bstride;
+      z_tile<BC, MODE, T>(V, ldv, F, N, f0, n0, Wb, Hs, K, ks, kappa, beta, Zn, Zd);
       __syncthreads();
-      const T* A1 = (MODE == PM_KKT) ? Ws : C1s;
+      const T* A1 = (MODE == PM_KKT) ? Wb : C1b;
 #pragma unroll 2
       for (int f4 = 0; f4 < ST_TF / 4; ++f4) {
         const double bn = Zn[(4 * f4 + t) * (ST_NC + 1) + 8 * c + g];
@@ -314,7 +355,7 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
             const double a1 = kk < K ? A1[(4 * f4 + t) * ks + kk] : 0.0;
             dmma884(dn[j], a1, bn);
             if (use_den) {
-              const double a2 = kk < K ? C2s[(4 * f4 + t) * ks + kk] : 0.0;
+              const double a2 = kk < K ? C2b[(4 * f4 + t) * ks + kk] : 0.0;
               dmma884(dd[j], a2, bd);
             }
           }

@@ -421,9 +421,9 @@ struct Engine : EngineBase {
 
   size_t smem_wside() const {
     int ks = kstride(K);
-    return size_t(ST_TF * ks + 3 * ST_NC * ks + 2 * ST_TF * (ST_NC + 1)) * sizeof(T);
+    return size_t(ST_TF * ks + hside_nbuf() * 3 * ST_NC * ks + 2 * ST_TF * (ST_NC + 1)) * sizeof(T);
   }
-  // the fp64 H-side pass double-buffers its row stage when two copies fit
+  // the fp64 passes double-buffer their row / column stage when two copies fit
   int hside_nbuf() const {
     if (!std::is_same<T, double>::value) return 1;
     int ks = kstride(K);
@@ -442,7 +442,7 @@ struct Engine : EngineBase {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
     dim3 grid((F + ST_TF - 1) / ST_TF, S);
     kern<<<grid, ST_THREADS, sm, stream>>>(V, ldv, F, N, K, Wp, Hp, C1, C2, seg_cols, sc,
-                                           wpart, st, slot);
+                                           wpart, hside_nbuf(), st, slot);
     CK(cudaGetLastError());
     launches += 1;
     return 0;

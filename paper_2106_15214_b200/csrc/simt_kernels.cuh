@@ -156,16 +156,17 @@ __global__ void __launch_bounds__(ST_THREADS)
 wside_partials(const T* __restrict__ V, size_t ldv, int F, int N, int K,
                const T* __restrict__ Wp, const T* __restrict__ Hp,
                const T* __restrict__ C1, const T* __restrict__ C2,
-               int seg_cols, Scalars sc, double* __restrict__ part,
+               int seg_cols, Scalars sc, double* __restrict__ part, int nbuf,
                const RunState* st, int slot) {
   if (!iter_active(st, slot)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int ks = kstride(K);
+  // nbuf (1 or 2) copies of the column stage [Hs | C1s | C2s]; two when they fit (fp64 path)
   T* Ws = reinterpret_cast<T*>(smem_raw);
   T* Hs = Ws + ST_TF * ks;
   T* C1s = Hs + ST_NC * ks;
   T* C2s = C1s + ST_NC * ks;
-  T* Zn = C2s + ST_NC * ks;
+  T* Zn = Hs + nbuf * 3 * ST_NC * ks;
   T* Zd = Zn + ST_TF * (ST_NC + 1);
 
   const int f0 = blockIdx.x * ST_TF;
@@ -185,14 +186,33 @@ wside_partials(const T* __restrict__ V, size_t ldv, int F, int N, int K,
     double dn[NJ][2], dd[NJ][2];
 #pragma unroll
     for (int j = 0; j < NJ; ++j) { dn[j][0] = dn[j][1] = 0.0; dd[j][0] = dd[j][1] = 0.0; }
-    for (int n0 = nbeg; n0 < nend; n0 += ST_NC) {
+    const int bstride = 3 * ST_NC * ks;   // doubles between the two column stages
+    auto stage = [&](int n0, int b) {
+      const int valid = min(ST_NC, nend - n0);
+      load_rows_async(Hs + b * bstride, Hp + (size_t)n0 * K, ST_NC, valid, K, ks);
+      load_rows_async(C1s + b * bstride, C1 + (size_t)n0 * K, ST_NC, valid, K, ks);
+      if (MODE != PM_KKT) load_rows_async(C2s + b * bstride, C2 + (size_t)n0 * K, ST_NC, valid, K, ks);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (nbuf == 2 && nbeg < nend) stage(nbeg, 0);
+    int it = 0;
+    for (int n0 = nbeg; n0 < nend; n0 += ST_NC, ++it) {
+      const int b = nbuf == 2 ? (it & 1) : 0;
+      __syncthreads();   // the previous step's products have read the other stage and Zn / Zd
+      if (nbuf == 2) {
+        const bool more = n0 + ST_NC < nend;
+        if (more) stage(n0 + ST_NC, b ^ 1);
+        if (more) asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else asm volatile("cp.async.wait_group 0;" ::: "memory");
+      } else {
+        stage(n0, 0);
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
       __syncthreads();
-      int valid = min(ST_NC, nend - n0);
-      load_rows(Hs, Hp + (size_t)n0 * K, ST_NC, valid, K, ks);
-      load_rows(C1s, C1 + (size_t)n0 * K, ST_NC, valid, K, ks);
-      if (MODE != PM_KKT) load_rows(C2s, C2 + (size_t)n0 * K, ST_NC, valid, K, ks);
-      __syncthreads();
-      z_tile<BC, MODE, T>(V, ldv, F, nend, f0, n0, Ws, Hs, K, ks, kappa, beta, Zn, Zd);
+      const double* Hb = Hs + b * bstride;
+      const double* C1b = C1s + b * bstride;
+      const double* C2b = C2s + b * bstride;
+      z_tile<BC, MODE, T>(V, ldv, F, nend, f0, n0, Ws, Hb, K, ks, kappa, beta, Zn, Zd);
       __syncthreads();
 #pragma unroll 2
       for (int n4 = 0; n4 < ST_NC / 4; ++n4) {
@@ -202,10 +222,10 @@ wside_partials(const T* __restrict__ V, size_t ldv, int F, int N, int K,
         for (int j = 0; j < NJ; ++j) {
           const int kk = 8 * (kp + 2 * j) + g;
           if (8 * (kp + 2 * j) < K) {
-            const double b1 = kk < K ? C1s[(4 * n4 + t) * ks + kk] : 0.0;
+            const double b1 = kk < K ? C1b[(4 * n4 + t) * ks + kk] : 0.0;
             dmma884(dn[j], an, b1);
             if (MODE != PM_KKT) {
-              const double b2 = kk < K ? C2s[(4 * n4 + t) * ks + kk] : 0.0;
+              const double b2 = kk < K ? C2b[(4 * n4 + t) * ks + kk] : 0.0;
               dmma884(dd[j], ad, b2);
             }
           }

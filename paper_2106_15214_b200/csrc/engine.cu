@@ -433,7 +433,7 @@ struct Engine : EngineBase {
     int ks = kstride(K);
     return size_t(ST_NC * ks + hside_nbuf() * 3 * ST_TF * ks + 2 * ST_TF * (ST_NC + 1)) * sizeof(T);
   }
-  size_t smem_obj() const { return size_t((ST_TF + ST_NC) * kstride(K)) * sizeof(T); }
+  size_t smem_obj() const { return size_t((ST_TF + 2 * ST_NC) * kstride(K)) * sizeof(T); }   // two H~ stages (fp64)
 
   template <int BC, int MODE>
   int launch_wside(const T* Wp, const T* Hp, const T* C1, const T* C2, int slot) {

@@ -506,21 +506,43 @@ objective_partials(const T* __restrict__ V, size_t ldv, int F, int N, int K,
   const T kappa = T(sc.kappa);
   load_rows(Ws, W + (size_t)f0 * K, ST_TF, F - f0, K, ks);
   double s = 0.0;
-  for (int n0 = nbeg; n0 < nend; n0 += ST_NC) {
-    __syncthreads();
-    load_rows(Hs, Ht + (size_t)n0 * K, ST_NC, min(ST_NC, nend - n0), K, ks);
-    __syncthreads();
-    if constexpr (std::is_same<T, double>::value) {
-      const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-      const int r = w & 3, cp = w >> 2, g = lane >> 2, t = lane & 3;
+  if constexpr (std::is_same<T, double>::value) {
+    // fp64: the H~ rows of the next 32 columns arrive (cp.async, second stage) while this step
+    // forms its model tile; the V values are requested before the product chain
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = w & 3, cp = w >> 2, g = lane >> 2, t = lane & 3;
+    const int bstride = ST_NC * ks;
+    auto stage = [&](int n0, int b) {
+      load_rows_async(Hs + b * bstride, Ht + (size_t)n0 * K, ST_NC, min(ST_NC, nend - n0), K, ks);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (nbeg < nend) stage(nbeg, 0);
+    int it = 0;
+    for (int n0 = nbeg; n0 < nend; n0 += ST_NC, ++it) {
+      const int b = it & 1;
+      __syncthreads();   // the previous step has read the other stage
+      const bool more = n0 + ST_NC < nend;
+      if (more) stage(n0 + ST_NC, b ^ 1);
+      if (more) asm volatile("cp.async.wait_group 1;" ::: "memory");
+      else asm volatile("cp.async.wait_group 0;" ::: "memory");
+      double xv[2][2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int f = 8 * r + g, n = 8 * (2 * cp + c) + 2 * t + e;
+          xv[c][e] = (f0 + f < F && n0 + n < nend) ? double(V[(size_t)(f0 + f) * ldv + n0 + n]) : 0.0;
+        }
+      __syncthreads();
+      const double* Hb = Hs + b * bstride;
       double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
       for (int k0 = 0; k0 < K; k0 += 4) {
         const int k = k0 + t;
         const double a = k < K ? Ws[(8 * r + g) * ks + k] : 0.0;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          const double b = k < K ? Hs[(8 * (2 * cp + c) + g) * ks + k] : 0.0;
-          dmma884(acc[c], a, b);
+          const double bb = k < K ? Hb[(8 * (2 * cp + c) + g) * ks + k] : 0.0;
+          dmma884(acc[c], a, bb);
         }
       }
 #pragma unroll
@@ -528,13 +550,15 @@ objective_partials(const T* __restrict__ V, size_t ldv, int F, int N, int K,
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int f = 8 * r + g, n = 8 * (2 * cp + c) + 2 * t + e;
-          if (f0 + f < F && n0 + n < nend) {
-            const double x = double(V[(size_t)(f0 + f) * ldv + n0 + n]);
-            s += divergence<BC>(x, acc[c][e] + double(kappa), sc.beta);
-          }
+          if (f0 + f < F && n0 + n < nend)
+            s += divergence<BC>(xv[c][e], acc[c][e] + double(kappa), sc.beta);
         }
-      continue;
     }
+  }
+  for (int n0 = nbeg; n0 < nend && !std::is_same<T, double>::value; n0 += ST_NC) {
+    __syncthreads();
+    load_rows(Hs, Ht + (size_t)n0 * K, ST_NC, min(ST_NC, nend - n0), K, ks);
+    __syncthreads();
     for (int e = threadIdx.x; e < ST_TF * ST_NC; e += blockDim.x) {
       int f = e / ST_NC, n = e - f * ST_NC;
       if (f0 + f < F && n0 + n < nend) {

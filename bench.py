@@ -81,6 +81,11 @@ def make_init(cfg_id, n0, n1):
     return w0, np.ascontiguousarray(h0[:, n0:n1])
 
 
+# measured tensor peaks (tools/tensor_peaks.cu, profiles/r02_tensor_peaks.txt): the fp32 passes
+# run 3xTF32 products on tcgen05 (a third of the dense TF32 rate), the fp64 kernels run DMMA
+TENSOR_PEAK_TFLOPS = {"fp32": 1114.4 / 3.0, "fp64": 37.11}
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -472,9 +477,22 @@ def main():
         "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
         "algorithmic_bytes_per_launch": vbytes_local,
         "launch_ms": pass_ms, "launch_samples": pass_samples,
-        "iteration_roofline_ms": c["F"] * c["N"] * esize / world / (hbm * 1e9) * 1e3,
-        "iteration_frac": (c["F"] * c["N"] * esize / world / (hbm * 1e9) * 1e3) / (ms / args.steps),
     }
+    # iteration roofline of BASELINE.md section 3: the slower of reading V once at HBM bandwidth
+    # and 10 F N K flops at the tensor peak of the arithmetic the pass runs in, measured on this
+    # pool's B200 with tools/tensor_peaks.cu (profiles/r02_tensor_peaks.txt)
+    t_hbm = c["F"] * c["N"] * esize / world / (hbm * 1e9) * 1e3
+    t_tc = 10.0 * c["F"] * c["N"] * c["K"] / world / (TENSOR_PEAK_TFLOPS[c["dtype"]] * 1e12) * 1e3
+    roofline.update({
+        "iteration_roofline_ms": max(t_hbm, t_tc),
+        "iteration_frac": max(t_hbm, t_tc) / (ms / args.steps),
+        "iteration_hbm_ms": t_hbm, "iteration_tensor_ms": t_tc,
+        "iteration_bound": "hbm" if t_hbm >= t_tc else "tensor",
+        "tensor_peak_tflops": TENSOR_PEAK_TFLOPS[c["dtype"]],
+        "tensor_peak_source": "tools/tensor_peaks.cu on this pool's B200 "
+                              "(profiles/r02_tensor_peaks.txt): tcgen05 kind::tf32 1114.4 TFLOP/s "
+                              "dense / 3 for 3xTF32; mma.sync.m8n8k4.f64 37.1 TFLOP/s",
+    })
     out = {
         "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,

@@ -117,6 +117,7 @@ struct Engine : EngineBase {
   int bc = BC_GEN;
   int L = 1, Lw = 1, Lh = 1;
   bool begun = false;
+  bool chi_h_valid = false;   // C1h / C2h hold chi(H~, H~) of the live iterate (reference-order JMM)
   cudaGraphExec_t gexec = nullptr;
   int gchunk = 0;
   int launches = 0;
@@ -366,6 +367,7 @@ struct Engine : EngineBase {
     if (!V) return fail(BNMF_E_STATE, "set_dense must precede set_factors");
     if (K_ < 1) return fail(BNMF_E_ARG, "rank must be positive");
     CK(cudaSetDevice(device));
+    chi_h_valid = false;
     if (int rc = alloc_factors(int(K_))) return rc;
     size_t fk = size_t(F) * K, nk = size_t(N) * K;
     if (int rc = ensure_staging(std::max(fk, nk) * sizeof(double))) return rc;
@@ -512,10 +514,19 @@ struct Engine : EngineBase {
   }
 
   // W-side: partials -> segment reduction -> (allreduce) -> update
+  // c1o / c2o (optional): chi maps of the new W against `base` (the JMM H-side factors)
   int w_update(const T* Wp, const T* Hp, const T* C1, const T* C2, const T* base, T* out,
-               int slot) {
+               int slot, T* c1o = nullptr, T* c2o = nullptr) {
     size_t fk = size_t(F) * K;
     if (int rc = wside(PM_UPDATE, Wp, Hp, C1, C2, slot)) return rc;
+    if (nranks == 1) {
+      // one rank: segment reduction, update and chi maps in one launch
+      reduce_update_w<T><<<grid_for(fk), 256, 0, stream>>>(wpart, 2 * fk, S, base, F, K, out, c1o,
+                                                          c2o, comm, sc, st, slot);
+      CK(cudaGetLastError());
+      launches += 1;
+      return 0;
+    }
     reduce_segments<<<grid_for(2 * fk), 256, 0, stream>>>(wpart, 2 * fk, S, 2 * fk, comm, st,
                                                            slot);
     CK(cudaGetLastError());
@@ -525,6 +536,7 @@ struct Engine : EngineBase {
                                                    slot);
     CK(cudaGetLastError());
     launches += 1;
+    if (c1o) return chi(out, base, c1o, c2o, fk, slot);
     return 0;
   }
 
@@ -536,6 +548,8 @@ struct Engine : EngineBase {
   }
 
   int colsums(const T* M, int slot) {
+    // fp64: hside_pass adds the columns of its C2 operand itself (same row order)
+    if (std::is_same<T, double>::value) return 0;
     // K <= 128 (the engine's rank cap) < CS_THREADS
     const size_t row_bytes = size_t(K) * sizeof(T);
     const int rows = int(std::max<size_t>(1, std::min<size_t>(size_t(F), CS_SMEM_MAX / row_bytes)));
@@ -563,9 +577,10 @@ struct Engine : EngineBase {
     if (p.algorithm == BNMF_JMM) {
       for (int l = 0; l < L; ++l) {
         // chi maps of the moving H against the anchor (updates.py:217-218)
-        if ((rc = chi(l == 0 ? Ht : Hc, Ht, C1h, C2h, nk, slot))) return rc;
-        if ((rc = w_update(Wt, Ht, C1h, C2h, Wt, Wc, slot))) return rc;
-        if ((rc = chi(Wc, Wt, C1w, C2w, fk, slot))) return rc;
+        // (at l == 0 they are chi(H~, H~), written by scale_h_chi of the previous iteration
+        // or by step() before the first one)
+        if (l > 0 && (rc = chi(Hc, Ht, C1h, C2h, nk, slot))) return rc;
+        if ((rc = w_update(Wt, Ht, C1h, C2h, Wt, Wc, slot, C1w, C2w))) return rc;
         if (den_ones && (rc = colsums(C2w, slot))) return rc;
         if (l == 0 && (rc = prof_mark(true, slot))) return rc;
         if ((rc = hside(PM_UPDATE, Wt, Ht, C1w, C2w, Ht, Hc, den_ones, slot))) return rc;
@@ -587,16 +602,26 @@ struct Engine : EngineBase {
     // objective of the unnormalised new iterate (solver.py:304-309)
     if ((rc = objective(Wc, Hc, slot))) return rc;
     double* obj = comm + 2 * fk;
-    sum_small<<<1, 1024, 0, stream>>>(opart, n_oblocks, obj, st, slot);
-    CK(cudaGetLastError());
-    launches += 1;
-    if ((rc = allreduce(obj, 1))) return rc;
+    if (nranks > 1) {
+      sum_small<<<1, 1024, 0, stream>>>(opart, n_oblocks, obj, st, slot);
+      CK(cudaGetLastError());
+      launches += 1;
+      if ((rc = allreduce(obj, 1))) return rc;
+    }
     // normalise (solver.py:311, 167-171)
     normalize_w<T><<<K, 32, 0, stream>>>(Wc, F, K, Wt, norms, st, slot);
     CK(cudaGetLastError());
-    scale_h<T><<<grid_for(nk), 256, 0, stream>>>(Hc, size_t(N), K, norms, Ht, st, slot);
+    if (p.algorithm == BNMF_JMM)
+      scale_h_chi<T><<<grid_for(nk), 256, 0, stream>>>(Hc, size_t(N), K, norms, Ht, C1h, C2h, sc,
+                                                      st, slot);
+    else
+      scale_h<T><<<grid_for(nk), 256, 0, stream>>>(Hc, size_t(N), K, norms, Ht, st, slot);
     CK(cudaGetLastError());
-    finish_iter<<<1, 1, 0, stream>>>(st, slot, obj, tr_obj, tr_sec, sc.tol);
+    if (nranks > 1)
+      finish_iter<<<1, 1, 0, stream>>>(st, slot, obj, tr_obj, tr_sec, sc.tol);
+    else
+      finish_iter_sum<<<1, 1024, 0, stream>>>(st, slot, opart, n_oblocks, obj, tr_obj, tr_sec,
+                                              sc.tol);
     CK(cudaGetLastError());
     launches += 3;
     if (p.compute_kkt) {
@@ -704,6 +729,7 @@ struct Engine : EngineBase {
     // capture, so the graph and the direct path agree)
     CK(cudaStreamSynchronize(stream));
     begun = true;
+    chi_h_valid = false;
     return 0;
   }
 
@@ -739,6 +765,11 @@ struct Engine : EngineBase {
   int step(int64_t n) override {
     if (!begun) return fail(BNMF_E_STATE, "begin must precede step");
     CK(cudaSetDevice(device));
+    if (!fused_active && p.algorithm == BNMF_JMM && !chi_h_valid) {
+      // W-side factors chi(H~, H~) of the first iteration; later ones come from scale_h_chi
+      if (int rc = chi(Ht, Ht, C1h, C2h, size_t(N) * K, 0)) return rc;
+      chi_h_valid = true;
+    }
     const int chunk = kChunk;
     int64_t full = n / chunk, rest = n % chunk;
     if (full > 0) {
@@ -857,6 +888,7 @@ struct Engine : EngineBase {
         h_out = true;
         break;
       case BNMF_OP_JMM_W:
+        chi_h_valid = false;
         if ((rc = chi(Hc, Ht, C1h, C2h, nk, 0))) return rc;
         if ((rc = w_update(Wt, Ht, C1h, C2h, Wt, Wc, 0))) return rc;
         w_out = true;

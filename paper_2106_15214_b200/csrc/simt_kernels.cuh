@@ -332,6 +332,11 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
 #pragma unroll
     for (int j = 0; j < NJ; ++j) { dn[j][0] = dn[j][1] = 0.0; dd[j][0] = dd[j][1] = 0.0; }
     const bool use_den = (MODE != PM_KKT) && !den_ones;
+    // beta = 1 denominators: colsum(C2w), accumulated here from the staged C2 rows (thread k
+    // adds rows 0, 1, ... in order, numpy's order, like the separate col_sums launch it replaces)
+    const bool fold_cs = (MODE != PM_KKT) && den_ones;
+    __shared__ double s_cs[ST_KMAX];
+    double cs = 0.0;
     const int bstride = 3 * ST_TF * ks;   // doubles between the two row stages
     // rows of tile f0 into stage b, one cp.async group
     auto stage = [&](int f0, int b) {
@@ -339,7 +344,8 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
       load_rows_async(Ws + b * bstride, Wp + (size_t)f0 * K, ST_TF, valid_f, K, ks);
       if (MODE != PM_KKT) {
         load_rows_async(C1s + b * bstride, C1w + (size_t)f0 * K, ST_TF, valid_f, K, ks);
-        if (use_den) load_rows_async(C2s + b * bstride, C2w + (size_t)f0 * K, ST_TF, valid_f, K, ks);
+        if (use_den || fold_cs)
+          load_rows_async(C2s + b * bstride, C2w + (size_t)f0 * K, ST_TF, valid_f, K, ks);
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -362,6 +368,10 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
       const double* C1b = C1s + b * bstride;
       const double* C2b = C2s + b * bstride;
       z_tile<BC, MODE, T>(V, ldv, F, N, f0, n0, Wb, Hs, K, ks, kappa, beta, Zn, Zd);
+      if (fold_cs && threadIdx.x < K) {
+        const int vf = min(ST_TF, F - f0);
+        for (int r = 0; r < vf; ++r) cs += C2b[r * ks + threadIdx.x];
+      }
       __syncthreads();
       const T* A1 = (MODE == PM_KKT) ? Wb : C1b;
 #pragma unroll 2
@@ -401,13 +411,17 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
       }
       return;
     }
+    if (fold_cs) {
+      if (threadIdx.x < K) s_cs[threadIdx.x] = cs;
+      __syncthreads();
+    }
 #pragma unroll
     for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int k = 8 * (kp + 2 * j) + g, n = 8 * c + 2 * t + e;
         if (k < K && n < valid_n) {
-          const double den = den_ones ? colsum_c2[k] : dd[j][e];
+          const double den = den_ones ? s_cs[k] : dd[j][e];
           const double rr = dn[j][e] / fmax(den, sc.floor);
           const double b = double(Hbase[(size_t)(n0 + n) * K + k]);
           Hout[(size_t)(n0 + n) * K + k] = T(b * apply_exponent<double>(rr, sc.gamma));

@@ -67,6 +67,35 @@ __global__ void update_w(const T* __restrict__ base, const double* __restrict__ 
   }
 }
 
+// reduce_segments + update_w in one launch (one rank: no allreduce between them), optionally
+// with the chi maps of the new W against its base (the JMM H-side factors, updates.py:97-107).
+// The segment sums are added in the order reduce_segments uses, so the result is bitwise the
+// same as the three launches it replaces.
+template <typename T>
+__global__ void reduce_update_w(const double* __restrict__ part, size_t stride, int S,
+                                const T* __restrict__ base, int F, int K, T* __restrict__ out,
+                                T* __restrict__ c1, T* __restrict__ c2, double* __restrict__ sums,
+                                Scalars sc, const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  const int fk = F * K;
+  const T beta = T(sc.beta);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < fk; i += gridDim.x * blockDim.x) {
+    double num = 0.0, den = 0.0;
+    for (int k = 0; k < S; ++k) {
+      num += part[(size_t)k * stride + i];
+      den += part[(size_t)k * stride + fk + i];
+    }
+    sums[i] = num;
+    sums[fk + i] = den;
+    const double r = num / fmax(den, sc.floor);
+    const T b = base[i];
+    const T w = T(double(b) * apply_exponent<double>(r, sc.gamma));
+    out[i] = w;
+    if (c1) c1[i] = chi1<T>(w, b, beta);
+    if (c2) c2[i] = chi2<T>(w, b, beta);
+  }
+}
+
 // Column sums of an F x K matrix -> double K-vector, one thread per column, rows added in
 // order: the order of numpy's sum over axis 0, so that the beta = 1 denominators (and the
 // exact-equality stop rule that can hang on their last bit) match the reference bit for bit.
@@ -140,6 +169,26 @@ __global__ void scale_h(const T* __restrict__ H, size_t N, int K, const double* 
   }
 }
 
+// scale_h plus the chi maps of the rescaled H against itself: the W-side factors of the next
+// JMM iteration at its first sub-iteration (chi(H~, H~), updates.py:217-218)
+template <typename T>
+__global__ void scale_h_chi(const T* __restrict__ H, size_t N, int K,
+                            const double* __restrict__ norms, T* __restrict__ Hn,
+                            T* __restrict__ c1, T* __restrict__ c2, Scalars sc,
+                            const RunState* st, int slot) {
+  if (!iter_active(st, slot)) return;
+  const T beta = T(sc.beta);
+  size_t count = N * (size_t)K;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x) {
+    int k = int(i % K);
+    const T h = T(double(H[i]) * norms[k]);
+    Hn[i] = h;
+    c1[i] = chi1<T>(h, h, beta);
+    c2[i] = chi2<T>(h, h, beta);
+  }
+}
+
 // Mark the start of an iteration (timer, solver.py:302).
 static __global__ void begin_iter(RunState* st, int slot) {
   if (!iter_active(st, slot)) return;
@@ -169,6 +218,42 @@ static __global__ void finish_iter(RunState* st, int slot, const double* __restr
   st->iters_done = it;
 #ifdef BNMF_X_NOSTOP
   stop = false;   // timing experiments with garbage numerics
+#endif
+  if (stop) { st->stop_iter = it; st->converged = 1; }
+}
+
+// sum_small + finish_iter in one launch (one rank: no allreduce of the objective between them)
+static __global__ void finish_iter_sum(RunState* st, int slot, const double* __restrict__ in,
+                                       int count, double* __restrict__ obj,
+                                       double* __restrict__ trace_obj,
+                                       double* __restrict__ trace_sec, double tol) {
+  if (!iter_active(st, slot)) return;
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) s += in[i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double o = 0.0;
+  for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) o += red[w];
+  *obj = o;
+  long long it = st->base + slot;
+  bool stop = false;
+  if (it > 1) {
+    double prev = st->prev_obj;
+    if (o == prev) stop = true;
+    else if (o <= 0.0) stop = false;
+    else stop = (prev - o) / o <= tol;
+  }
+  unsigned long long t = globaltimer();
+  st->elapsed += double(t - st->t_begin) * 1e-9;
+  trace_obj[it - 1] = o;
+  trace_sec[it - 1] = st->elapsed;
+  st->prev_obj = o;
+  st->iters_done = it;
+#ifdef BNMF_X_NOSTOP
+  stop = false;
 #endif
   if (stop) { st->stop_iter = it; st->converged = 1; }
 }

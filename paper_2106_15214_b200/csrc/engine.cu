@@ -112,6 +112,7 @@ struct Engine : EngineBase {
   // schedule
   int S = 1, seg_cols = 32;
   int n_hblocks = 1, n_oblocks = 1;
+  int num_sms = 148;
   bnmf_params p{};
   Scalars sc{};
   int bc = BC_GEN;
@@ -129,7 +130,12 @@ struct Engine : EngineBase {
   bool prof = false;
   int prof_slots = 0;
 
-  explicit Engine(int dev, int dt) { device = dev; dtype = dt; }
+  explicit Engine(int dev, int dt) {
+    device = dev;
+    dtype = dt;
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0) num_sms = n;
+  }
 
   int prof_mark(bool start, int slot) {
     if (!prof || slot >= kChunk) return 0;
@@ -431,6 +437,17 @@ struct Engine : EngineBase {
     int ks = kstride(K);
     return size_t(ST_NC * ks + 6 * ST_TF * ks + 2 * ST_TF * (ST_NC + 1)) * sizeof(T) <= 200 * 1024 ? 2 : 1;
   }
+  // CTAs per column block of the fp64 H-side pass: with fewer column blocks than SMs the pass is
+  // bound by the latency of one block's walk over all F rows, so the rows are split over a
+  // cluster (the largest of 4, 2 that still fits two CTAs per SM and leaves >= 2 tiles each)
+  int hside_cluster() const {
+    if (!std::is_same<T, double>::value) return 1;
+    if (const char* e = getenv("BNMF_HSIDE_CLUSTER")) return std::max(1, atoi(e)) > 1 ? (atoi(e) >= 4 ? 4 : 2) : 1;
+    const int ntile = (F + ST_TF - 1) / ST_TF;
+    for (int c : {4, 2})
+      if (n_hblocks * c <= 2 * num_sms && ntile >= 2 * c) return c;
+    return 1;
+  }
   size_t smem_hside() const {
     int ks = kstride(K);
     return size_t(ST_NC * ks + hside_nbuf() * 3 * ST_TF * ks + 2 * ST_TF * (ST_NC + 1)) * sizeof(T);
@@ -456,8 +473,31 @@ struct Engine : EngineBase {
     auto kern = hside_pass<BC, MODE, T>;
     size_t sm = smem_hside();
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-    kern<<<n_hblocks, ST_THREADS, sm, stream>>>(V, ldv, F, N, K, Wp, Hp, C1, C2, Hb, Ho, colsum,
-                                                den_ones, sc, hpart, hside_nbuf(), st, slot);
+    const int cs = hside_cluster();
+    if (cs > 1) {
+      // few column blocks (fp64): the rows of a block are split over a cluster of cs CTAs
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(unsigned(n_hblocks * cs));
+      cfg.blockDim = dim3(ST_THREADS);
+      cfg.dynamicSmemBytes = sm;
+      cfg.stream = stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = unsigned(cs);
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      const T* Vc = V;
+      const double* csum = colsum;
+      int nb = hside_nbuf();
+      const RunState* stc = st;
+      CK(cudaLaunchKernelEx(&cfg, kern, Vc, ldv, F, N, K, Wp, Hp, C1, C2, Hb, Ho, csum, den_ones,
+                            sc, hpart, nb, stc, slot));
+    } else {
+      kern<<<n_hblocks, ST_THREADS, sm, stream>>>(V, ldv, F, N, K, Wp, Hp, C1, C2, Hb, Ho, colsum,
+                                                  den_ones, sc, hpart, hside_nbuf(), st, slot);
+    }
     CK(cudaGetLastError());
     launches += 1;
     return 0;

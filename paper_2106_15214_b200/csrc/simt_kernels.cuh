@@ -13,6 +13,7 @@
 // 8 x 8 sub-tiles, accumulators in the D fragments; fp32 keeps the scalar FMA form.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <type_traits>
 
 #include "bnmf_common.cuh"
@@ -317,7 +318,12 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
   T* Zd = Zn + ST_TF * (ST_NC + 1);
   __shared__ double red[ST_THREADS / 32];
 
-  const int n0 = blockIdx.x * ST_NC;
+  // fp64 with few column blocks: the F rows of a block are split over a cluster of CS CTAs
+  // (launch attribute; 1 otherwise), rank 0 adds the partial sums over DSMEM and updates
+  cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+  const int CS = int(cl.num_blocks()), cr = int(cl.block_rank());
+  const int hb = blockIdx.x / CS;
+  const int n0 = hb * ST_NC;
   const int valid_n = min(ST_NC, N - n0);
   const T kappa = T(sc.kappa), beta = T(sc.beta);
   load_rows(Hs, Hp + (size_t)n0 * K, ST_NC, valid_n, K, ks);
@@ -349,13 +355,15 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    if (nbuf == 2) stage(0, 0);
+    const int ntile = (F + ST_TF - 1) / ST_TF, per = (ntile + CS - 1) / CS;
+    const int fbeg = min(F, cr * per * ST_TF), fend = min(F, (cr + 1) * per * ST_TF);
+    if (nbuf == 2 && fbeg < fend) stage(fbeg, 0);
     int it = 0;
-    for (int f0 = 0; f0 < F; f0 += ST_TF, ++it) {
+    for (int f0 = fbeg; f0 < fend; f0 += ST_TF, ++it) {
       const int b = nbuf == 2 ? (it & 1) : 0;
       __syncthreads();   // the previous tile's products have read the other stage and Zn / Zd
       if (nbuf == 2) {
-        const bool more = f0 + ST_TF < F;
+        const bool more = f0 + ST_TF < fend;
         if (more) stage(f0 + ST_TF, b ^ 1);
         if (more) asm volatile("cp.async.wait_group 1;" ::: "memory");
         else asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -392,6 +400,41 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
         }
       }
     }
+    if (CS > 1) {
+      // partial sums of this CTA's rows -> shared memory (the row stages are free now), one
+      // column per thread; rank 0 adds the peers' in rank order
+      __syncthreads();
+      double* P = reinterpret_cast<double*>(Ws);
+      const int NJA = (K + 15) / 16;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+        if (j < NJA) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            P[((0 * NJA + j) * 2 + e) * ST_THREADS + threadIdx.x] = dn[j][e];
+            P[((1 * NJA + j) * 2 + e) * ST_THREADS + threadIdx.x] = dd[j][e];
+          }
+        }
+      if (fold_cs && threadIdx.x < K) s_cs[threadIdx.x] = cs;
+      cl.sync();
+      if (cr == 0) {
+        for (int r = 1; r < CS; ++r) {
+          const double* Pr = cl.map_shared_rank(P, r);
+#pragma unroll
+          for (int j = 0; j < NJ; ++j)
+            if (j < NJA) {
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                dn[j][e] += Pr[((0 * NJA + j) * 2 + e) * ST_THREADS + threadIdx.x];
+                dd[j][e] += Pr[((1 * NJA + j) * 2 + e) * ST_THREADS + threadIdx.x];
+              }
+            }
+          if (fold_cs && threadIdx.x < K) cs += cl.map_shared_rank(s_cs, r)[threadIdx.x];
+        }
+      }
+      cl.sync();   // the peers' shared memory stays valid until rank 0 has read it
+      if (cr != 0) return;
+    }
     if (MODE == PM_KKT) {
       double s = 0.0;
 #pragma unroll
@@ -407,7 +450,7 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
       if (threadIdx.x == 0) {
         double tt = 0.0;
         for (int ww = 0; ww < ST_THREADS / 32; ++ww) tt += red[ww];
-        part[blockIdx.x] = tt;
+        part[hb] = tt;
       }
       return;
     }
@@ -480,7 +523,7 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
     if (threadIdx.x == 0) {
       double t = 0.0;
       for (int w = 0; w < ST_THREADS / 32; ++w) t += red[w];
-      part[blockIdx.x] = t;
+      part[hb] = t;
     }
     return;
   }

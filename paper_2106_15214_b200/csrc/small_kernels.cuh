@@ -81,6 +81,7 @@ __global__ void reduce_update_w(const double* __restrict__ part, size_t stride, 
   const T beta = T(sc.beta);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < fk; i += gridDim.x * blockDim.x) {
     double num = 0.0, den = 0.0;
+#pragma unroll 8
     for (int k = 0; k < S; ++k) {
       num += part[(size_t)k * stride + i];
       den += part[(size_t)k * stride + fk + i];

@@ -355,7 +355,11 @@ struct Engine : EngineBase {
     // segments of the W-side / objective passes: ~4 CTAs per SM
     int ftiles = (F + ST_TF - 1) / ST_TF;
     int ctiles = (N + ST_NC - 1) / ST_NC;
-    S = std::max(1, std::min(ctiles, (4 * 148 + ftiles - 1) / ftiles));
+    // (fp64: the DMMA passes hold ~125 registers and ~100 KB of stages, two CTAs per SM, and a
+    // grid beyond one wave only adds a tail)
+    int cps = std::is_same<T, double>::value ? 2 : 4;
+    if (const char* e = getenv("BNMF_WSIDE_CPS")) cps = std::max(1, atoi(e));
+    S = std::max(1, std::min(ctiles, (cps * num_sms + ftiles - 1) / ftiles));
     seg_cols = ((N + S - 1) / S + ST_NC - 1) / ST_NC * ST_NC;
     S = (N + seg_cols - 1) / seg_cols;
     n_hblocks = ctiles;
@@ -439,12 +443,12 @@ struct Engine : EngineBase {
   }
   // CTAs per column block of the fp64 H-side pass: with fewer column blocks than SMs the pass is
   // bound by the latency of one block's walk over all F rows, so the rows are split over a
-  // cluster (the largest of 4, 2 that still fits two CTAs per SM and leaves >= 2 tiles each)
+  // cluster (the largest of 4, 3, 2 that still fits two CTAs per SM and leaves >= 2 tiles each)
   int hside_cluster() const {
     if (!std::is_same<T, double>::value) return 1;
-    if (const char* e = getenv("BNMF_HSIDE_CLUSTER")) return std::max(1, atoi(e)) > 1 ? (atoi(e) >= 4 ? 4 : 2) : 1;
+    if (const char* e = getenv("BNMF_HSIDE_CLUSTER")) return std::min(8, std::max(1, atoi(e)));
     const int ntile = (F + ST_TF - 1) / ST_TF;
-    for (int c : {4, 2})
+    for (int c : {4, 3, 2})
       if (n_hblocks * c <= 2 * num_sms && ntile >= 2 * c) return c;
     return 1;
   }

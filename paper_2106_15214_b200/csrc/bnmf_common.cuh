@@ -61,6 +61,31 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// Objective bookkeeping + stop rule of iteration base + slot (solver.py:309-319, 174-180); one
+// thread.  o: the reduced objective (global, after any allreduce).
+__device__ __forceinline__ void finish_body(RunState* st, int slot, double o,
+                                            double* __restrict__ trace_obj,
+                                            double* __restrict__ trace_sec, double tol) {
+  long long it = st->base + slot;
+  bool stop = false;
+  if (it > 1) {
+    double prev = st->prev_obj;
+    if (o == prev) stop = true;
+    else if (o <= 0.0) stop = false;
+    else stop = (prev - o) / o <= tol;
+  }
+  unsigned long long t = globaltimer();
+  st->elapsed += double(t - st->t_begin) * 1e-9;
+  trace_obj[it - 1] = o;
+  trace_sec[it - 1] = st->elapsed;
+  st->prev_obj = o;
+  st->iters_done = it;
+#ifdef BNMF_X_NOSTOP
+  stop = false;   // timing experiments with garbage numerics
+#endif
+  if (stop) { st->stop_iter = it; st->converged = 1; }
+}
+
 // ---------------------------------------------------------------------------
 // Elementwise rules.  T is the storage/compute type (float or double).
 

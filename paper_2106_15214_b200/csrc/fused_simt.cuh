@@ -52,8 +52,12 @@ static __global__ void __launch_bounds__(1024) fused_update(const double* __rest
                              WPair Wt2, float* Wn, float* C1, float* C2, double* norms,
                              double* csum2,
                              int algorithm, int den_ones, Scalars sc, const RunState* st, int slot,
-                             int p_override) {
+                             int p_override, RunState* st_fin, double* tr_obj, double* tr_sec) {
   if (p_override < 0 && !iter_active(st, slot)) return;
+  // st_fin != nullptr: trace row and stop rule of this iteration (the finish_iter launch folded
+  // in; the objective sits behind the W sums in comm).  A stop leaves this slot active.
+  if (st_fin && blockIdx.x == 0 && threadIdx.x == 0)
+    finish_body(st_fin, slot, comm[(size_t)2 * F * K], tr_obj, tr_sec, sc.tol);
   const int par = iter_parity(st, slot, p_override);
   const float* Wcur = Wt2.w[par];    // W~_p
   float* Wnext = Wt2.w[par ^ 1];     // W~_{p+1}

@@ -448,17 +448,13 @@ static int enqueue_pass_and_update(FusedState* fs, const FusedIO& io, int slot, 
     if (r != ncclSuccess) { err = std::string("ncclAllReduce: ") + ncclGetErrorString(r); return -1; }
     if (io.launches) *io.launches += 1;
   }
-  if (finish) {
-    finish_iter<<<1, 1, 0, io.stream>>>(io.st, slot, io.comm + fk2, io.tr_obj, io.tr_sec,
-                                        io.sc.tol);
-    FCK(cudaGetLastError());
-    if (io.launches) *io.launches += 1;
-  }
+  // the trace row and stop rule of the iteration (finish_iter) ride in fused_update
   WPair wp;
   wp.w[0] = fs->W2[0]; wp.w[1] = fs->W2[1];
   fused_update<<<io.K, FU_THREADS, 0, io.stream>>>(io.comm, io.F, io.K, wp, fs->Wn, fs->C1, fs->C2,
                                             fs->norms, fs->csum2, io.algorithm, a.den_ones, io.sc,
-                                            io.st, slot, p_override);
+                                            io.st, slot, p_override, finish ? io.st : nullptr,
+                                            io.tr_obj, io.tr_sec);
   FCK(cudaGetLastError());
   if (io.launches) *io.launches += 1;
   return 0;

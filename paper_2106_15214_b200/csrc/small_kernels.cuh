@@ -202,25 +202,7 @@ static __global__ void finish_iter(RunState* st, int slot, const double* __restr
                             double* __restrict__ trace_obj, double* __restrict__ trace_sec,
                             double tol) {
   if (!iter_active(st, slot)) return;
-  long long it = st->base + slot;
-  double o = *obj;
-  bool stop = false;
-  if (it > 1) {
-    double prev = st->prev_obj;
-    if (o == prev) stop = true;
-    else if (o <= 0.0) stop = false;
-    else stop = (prev - o) / o <= tol;
-  }
-  unsigned long long t = globaltimer();
-  st->elapsed += double(t - st->t_begin) * 1e-9;
-  trace_obj[it - 1] = o;
-  trace_sec[it - 1] = st->elapsed;
-  st->prev_obj = o;
-  st->iters_done = it;
-#ifdef BNMF_X_NOSTOP
-  stop = false;   // timing experiments with garbage numerics
-#endif
-  if (stop) { st->stop_iter = it; st->converged = 1; }
+  finish_body(st, slot, *obj, trace_obj, trace_sec, tol);
 }
 
 // sum_small + finish_iter in one launch (one rank: no allreduce of the objective between them)
@@ -239,24 +221,7 @@ static __global__ void finish_iter_sum(RunState* st, int slot, const double* __r
   double o = 0.0;
   for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) o += red[w];
   *obj = o;
-  long long it = st->base + slot;
-  bool stop = false;
-  if (it > 1) {
-    double prev = st->prev_obj;
-    if (o == prev) stop = true;
-    else if (o <= 0.0) stop = false;
-    else stop = (prev - o) / o <= tol;
-  }
-  unsigned long long t = globaltimer();
-  st->elapsed += double(t - st->t_begin) * 1e-9;
-  trace_obj[it - 1] = o;
-  trace_sec[it - 1] = st->elapsed;
-  st->prev_obj = o;
-  st->iters_done = it;
-#ifdef BNMF_X_NOSTOP
-  stop = false;
-#endif
-  if (stop) { st->stop_iter = it; st->converged = 1; }
+  finish_body(st, slot, o, trace_obj, trace_sec, tol);
 }
 
 // res_W = sum |min(W, gradW)| / (F K)   (diagnostics.py:57)

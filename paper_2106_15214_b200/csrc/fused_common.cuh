@@ -38,6 +38,7 @@ struct FusedArgs {
   int kkt;                // 1 = KKT pass (H side only, no update): sum |min(H~_p, W~_p^T (Zd - Zn))|
                           // per CTA into opart (diagnostics.py:46-59); Wa = C1 = C2 = W~_p
   long long* prof;        // optional per-CTA wait-cycle counters [G][48] (BNMF_TC_PROF=1)
+  unsigned long long* tmark;  // RunState::t_begin when this launch opens a timed iteration, else null
   Scalars sc;
 };
 

@@ -210,6 +210,8 @@ template <int BC, int KJ>
 __global__ void __launch_bounds__(THREADS)
 hpass(FusedArgs a, const RunState* st, int slot, int p_override) {
   if (p_override < 0 && !iter_active(st, slot)) return;
+  // the H pass opens a timed iteration: the start of its timer (begin_iter folded in)
+  if (a.tmark && blockIdx.x == 0 && threadIdx.x == 0) *a.tmark = globaltimer();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int KS = 32 * KJ;
   constexpr bool DEN = BC != BC_1;   // beta = 1: den = colsum(C2) (updates.py:133-137)

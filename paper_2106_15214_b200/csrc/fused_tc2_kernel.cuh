@@ -102,6 +102,8 @@ __global__ void __launch_bounds__(NTHREADS2, 1)
 fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, int F0,
                const RunState* st, int slot, int p_override) {
   if (p_override < 0 && !iter_active(st, slot)) return;
+  // first kernel of an iteration: the start of its timer (begin_iter folded in, solver.py:302)
+  if (a.tmark && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *a.tmark = globaltimer();
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));

@@ -87,6 +87,9 @@ __global__ void __launch_bounds__(threads_of(FBC), 1)
 pass_tc3(FusedArgs a, const __grid_constant__ CUtensorMap mapV, float* __restrict__ hpart,
          const RunState* st, int slot, int p_override) {
   if (p_override < 0 && !iter_active(st, slot)) return;
+  // the H pass opens a timed iteration: the start of its timer (begin_iter folded in)
+  if (MODE == MODE_H && a.tmark && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+    *a.tmark = globaltimer();
   using L = Lay<KP>;
   constexpr int NT = teams_of(FBC);          // item teams
   constexpr int IW = 64 / NT;                // columns of an item

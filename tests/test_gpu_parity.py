@@ -63,6 +63,30 @@ def test_config1_full_fp64_jmm_200_iterations():
         assert all(b <= a * (1 + 1e-10) for a, b in zip(obj, obj[1:]))
 
 
+@pytest.mark.parametrize("beta,algo", [(1.0, "jmm"), (0.5, "jmm"), (2.0, "bmm")])
+def test_fp64_hside_cluster_row_split_matches_unsplit(monkeypatch, beta, algo):
+    """The fp64 H-side pass splits the rows of a column block over a thread-block cluster when
+    there are fewer column blocks than SMs (partials over DSMEM, rank 0 updates).  Every cluster
+    size must reproduce the unsplit pass (same sums, added per row range), KKT pass included."""
+    rng = np.random.default_rng(7)
+    f, n, k = 300, 450, 21        # 15 column blocks, 10 row tiles (the last one ragged)
+    v = rng.gamma(1.0, 1.0, (f, k)) @ rng.gamma(1.0, 1.0, (k, n)) + 1e-3
+    w0 = rng.uniform(0.1, 1.0, (f, k))
+    h0 = rng.uniform(0.1, 1.0, (k, n))
+    cfg = bn.SolverConfig(beta=beta, rank=k, algorithm=algo, tol=1e-300, max_outer_iters=12)
+    out = {}
+    for cs in (1, 2, 3, 4):
+        monkeypatch.setenv("BNMF_HSIDE_CLUSTER", str(cs))
+        res = bn.fit(v, cfg, init=(w0, h0))
+        out[cs] = (np.array([r.objective for r in res.trace]), res.factors.w, res.factors.h,
+                   np.array([[r.kkt_w, r.kkt_h] for r in res.trace]))
+    for cs in (2, 3, 4):
+        assert max_rel(out[cs][0], out[1][0]) <= 1e-12
+        assert max_rel(out[cs][1], out[1][1]) <= 1e-11
+        assert max_rel(out[cs][2], out[1][2]) <= 1e-11
+        np.testing.assert_allclose(out[cs][3], out[1][3], rtol=1e-9, atol=1e-15)
+
+
 CFG = {
     "cfg2p": (lambda s: s.config2(F=1024, N=1024, K=32), 32, 2.0, None),
     "cfg3p": (lambda s: s.config3(F=1025, N=1024, K=20), 20, 0.0, None),

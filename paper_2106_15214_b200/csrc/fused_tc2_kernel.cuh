@@ -426,13 +426,18 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
     // ---------------- H item: rows row0 + IW it + [0, IW) of column n0 + row (stage s) -------
     auto h_item = [&](int n0, int it, int s, uint32_t ph) {
       PTIME_BEGIN(t_it);
+      PTIME_BEGIN(t_p0);
       float x[EPT], y[EPT];
       PWAITA(full_a + 8 * s, ph, 2);
       const int r0 = IW * it;
       const uint32_t xa = sb + OFF_STAGE + s * STAGE_BYTES + (r0 & 31) * VROWB + row * 4;
 #pragma unroll
       for (int i = 0; i < EPT; ++i) x[i] = lds_f32(xa + i * VROWB);
+      PTIME_END(t_p0, 7);
+      PTIME_BEGIN(t_p1);
       take_tile(y, 0);
+      PTIME_END(t_p1, 8);
+      PTIME_BEGIN(t_p2);
       const bool full = n0 + BN <= N && (rows_full || r0 + IW <= FTr);
       const bool nok = n0 + row < N;
 #pragma unroll
@@ -454,7 +459,10 @@ fused_pass_tc2(FusedArgs a, const __grid_constant__ CUtensorMap mapV, int CL, in
         if (s4 == 0) wait_zfree();
         store_z(zcol + 32 * s4, zn, zd);
       }
+      PTIME_END(t_p2, 9);
+      PTIME_BEGIN(t_p3);
       give_z();
+      PTIME_END(t_p3, 10);
       PTIME_END(t_it, 5);
     };
 

@@ -29,7 +29,7 @@ roles = {
     0: ("TMA", {0: "empty"}),
     1: ("Vt issuer", {0: "hp", 1: "hn", 2: "dfree"}),
     2: ("side issuer", {0: "zfull", 1: "accfree", 2: "accwfree"}),
-    3: ("team0 q3", {0: "dfull(H)", 1: "dfull(W)", 2: "full(H)", 3: "full(W)", 4: "zfree", 5: "H items", 6: "W items"}),
+    3: ("team0 q3", {0: "dfull(H)", 1: "dfull(W)", 2: "full(H)", 3: "full(W)", 4: "zfree", 5: "H items", 6: "W items", 7: "  H: stage wait + x loads", 8: "  H: tile wait + tcgen05.ld", 9: "  H: Z arithmetic + stores (incl. zfree)", 10: "  H: wait::st + fence + arrive"}),
     7: ("team1 q3", {0: "dfull(H)", 1: "dfull(W)", 2: "full(H)", 3: "full(W)", 4: "zfree", 5: "H items", 6: "W items"}),
     4 * NT - 1: ("last team q3", {0: "dfull(H)", 1: "dfull(W)", 2: "full(H)", 3: "full(W)", 4: "zfree", 5: "H items", 6: "W items"}),
     NW - 4: ("U team q3", {0: "hpfree", 1: "acch", 2: "xempty", 3: "xfull", 4: "wdone", 5: "accw", 6: "  acch->sends issued", 7: "acch->hn chain (incl. xempty/xfull/wdone waits)", 8: "  acch->AccH read", 9: "  acch->ratio done", 10: "  acch->peer partial added"}),

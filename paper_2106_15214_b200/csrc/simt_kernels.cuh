@@ -187,6 +187,12 @@ wside_partials(const T* __restrict__ V, size_t ldv, int F, int N, int K,
     double dn[NJ][2], dd[NJ][2];
 #pragma unroll
     for (int j = 0; j < NJ; ++j) { dn[j][0] = dn[j][1] = 0.0; dd[j][0] = dd[j][1] = 0.0; }
+    // beta = 1: Z_den is all ones, so den[f, k] = sum_n C2[n, k] is the same for every row of the
+    // tile: thread k adds the staged C2 rows in column order instead of a second DMMA chain per
+    // row (a third of the pass's DMMA work)
+    constexpr bool ONES = (BC == BC_1) && (MODE == PM_UPDATE);
+    __shared__ double s_seg[ST_KMAX];
+    double segs = 0.0;
     const int bstride = 3 * ST_NC * ks;   // doubles between the two column stages
     auto stage = [&](int n0, int b) {
       const int valid = min(ST_NC, nend - n0);
@@ -214,6 +220,10 @@ wside_partials(const T* __restrict__ V, size_t ldv, int F, int N, int K,
       const double* C1b = C1s + b * bstride;
       const double* C2b = C2s + b * bstride;
       z_tile<BC, MODE, T>(V, ldv, F, nend, f0, n0, Ws, Hb, K, ks, kappa, beta, Zn, Zd);
+      if (ONES && threadIdx.x < K) {
+        const int vn = min(ST_NC, nend - n0);
+        for (int r2 = 0; r2 < vn; ++r2) segs += C2b[r2 * ks + threadIdx.x];
+      }
       __syncthreads();
 #pragma unroll 2
       for (int n4 = 0; n4 < ST_NC / 4; ++n4) {
@@ -225,13 +235,17 @@ wside_partials(const T* __restrict__ V, size_t ldv, int F, int N, int K,
           if (8 * (kp + 2 * j) < K) {
             const double b1 = kk < K ? C1b[(4 * n4 + t) * ks + kk] : 0.0;
             dmma884(dn[j], an, b1);
-            if (MODE != PM_KKT) {
+            if (MODE != PM_KKT && !ONES) {
               const double b2 = kk < K ? C2b[(4 * n4 + t) * ks + kk] : 0.0;
               dmma884(dd[j], ad, b2);
             }
           }
         }
       }
+    }
+    if (ONES) {
+      if (threadIdx.x < K) s_seg[threadIdx.x] = segs;
+      __syncthreads();
     }
     const int f = f0 + 8 * r + g;
     if (f < F) {
@@ -242,7 +256,7 @@ wside_partials(const T* __restrict__ V, size_t ldv, int F, int N, int K,
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int k = 8 * (kp + 2 * j) + 2 * t + e;
-          if (k < K) { pn[k] = dn[j][e]; pd[k] = dd[j][e]; }
+          if (k < K) { pn[k] = dn[j][e]; pd[k] = ONES ? s_seg[k] : dd[j][e]; }
         }
     }
     return;

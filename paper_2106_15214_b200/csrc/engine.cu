@@ -653,7 +653,7 @@ struct Engine : EngineBase {
       if ((rc = allreduce(obj, 1))) return rc;
     }
     // normalise (solver.py:311, 167-171)
-    normalize_w<T><<<K, 32, 0, stream>>>(Wc, F, K, Wt, norms, st, slot);
+    normalize_w<T><<<K, NW_THREADS, 0, stream>>>(Wc, F, K, Wt, norms, st, slot);
     CK(cudaGetLastError());
     if (p.algorithm == BNMF_JMM)
       scale_h_chi<T><<<grid_for(nk), 256, 0, stream>>>(Hc, size_t(N), K, norms, Ht, C1h, C2h, sc,

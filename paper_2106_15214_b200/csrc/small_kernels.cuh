@@ -139,21 +139,30 @@ col_sums(const T* __restrict__ M, int F, int K, double* __restrict__ out, int ro
 }
 
 // norms[k] = sqrt(sum_f W[f,k]^2); Wn = W / norms (solver.py:167-171).
-// One warp per column, fixed-order lane partition + shuffle tree.
+// One block of NW_THREADS per column: fixed-order thread partition, shuffle tree per warp, the
+// warp sums added in warp order.
+constexpr int NW_THREADS = 128;
 template <typename T>
-__global__ void normalize_w(const T* __restrict__ W, int F, int K, T* __restrict__ Wn,
-                            double* __restrict__ norms, const RunState* st, int slot) {
+__global__ void __launch_bounds__(NW_THREADS)
+normalize_w(const T* __restrict__ W, int F, int K, T* __restrict__ Wn,
+            double* __restrict__ norms, const RunState* st, int slot) {
   if (!iter_active(st, slot)) return;
+  __shared__ double red[NW_THREADS / 32];
   int k = blockIdx.x;
   double s = 0.0;
-  for (int f = threadIdx.x; f < F; f += 32) {
+  for (int f = threadIdx.x; f < F; f += NW_THREADS) {
     double w = double(W[(size_t)f * K + k]);
     s += w * w;
   }
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  double nrm = sqrt(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  double tot = 0.0;
+#pragma unroll
+  for (int w = 0; w < NW_THREADS / 32; ++w) tot += red[w];
+  double nrm = sqrt(tot);
   if (threadIdx.x == 0) norms[k] = nrm;
-  for (int f = threadIdx.x; f < F; f += 32)
+  for (int f = threadIdx.x; f < F; f += NW_THREADS)
     Wn[(size_t)f * K + k] = T(double(W[(size_t)f * K + k]) / nrm);
 }
 

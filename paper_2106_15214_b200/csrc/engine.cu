@@ -118,6 +118,13 @@ struct Engine : EngineBase {
   int bc = BC_GEN;
   int L = 1, Lw = 1, Lh = 1;
   bool begun = false;
+  // fp64 JMM: Z tiles of the W-side pass kept for the H-side pass of the same outer iteration
+  // (F x ldz each; allocated when they fit ZSHARE_MAX_BYTES), zs_use: 1 = write, 2 = read
+  static constexpr size_t ZSHARE_MAX_BYTES = size_t(1) << 30;
+  T* Zgn = nullptr;
+  T* Zgd = nullptr;
+  size_t ldz = 0;
+  int zs_use = 0;
   bool chi_h_valid = false;   // C1h / C2h hold chi(H~, H~) of the live iterate (reference-order JMM)
   cudaGraphExec_t gexec = nullptr;
   int gchunk = 0;
@@ -150,7 +157,7 @@ struct Engine : EngineBase {
       if (ev_a[i]) cudaEventDestroy(ev_a[i]);
       if (ev_b[i]) cudaEventDestroy(ev_b[i]);
     }
-    T* tp[] = {V, Wt, Wc, Ht, Hc, C1h, C2h, C1w, C2w};
+    T* tp[] = {V, Wt, Wc, Ht, Hc, C1h, C2h, C1w, C2w, Zgn, Zgd};
     for (T* q : tp) if (q) cudaFree(q);
     double* dp[] = {wpart, comm, opart, hpart, norms, colsum, tr_obj, tr_sec, tr_kkt};
     for (double* q : dp) if (q) cudaFree(q);
@@ -337,7 +344,7 @@ struct Engine : EngineBase {
   int aF = 0, aN = 0;
   int alloc_factors(int K_) {
     if (K == K_ && F == aF && N == aN && Wt) return 0;
-    T** tp[] = {&Wt, &Wc, &Ht, &Hc, &C1h, &C2h, &C1w, &C2w};
+    T** tp[] = {&Wt, &Wc, &Ht, &Hc, &C1h, &C2h, &C1w, &C2w, &Zgn, &Zgd};
     for (T** q : tp) if (*q) { CK(cudaFree(*q)); *q = nullptr; }
     double** dp[] = {&wpart, &comm, &opart, &hpart, &norms, &colsum};
     for (double** q : dp) if (*q) { CK(cudaFree(*q)); *q = nullptr; }
@@ -370,6 +377,14 @@ struct Engine : EngineBase {
     CK(cudaMalloc(&hpart, size_t(n_hblocks) * sizeof(double)));
     CK(cudaMalloc(&norms, size_t(K) * sizeof(double)));
     CK(cudaMalloc(&colsum, size_t(K) * sizeof(double)));
+    // fp64: room for the Z tiles the W-side pass hands to the H-side pass (JMM); large inputs
+    // recompute them instead
+    ldz = (size_t(N) + 3) / 4 * 4;
+    if (std::is_same<T, double>::value && getenv("BNMF_NO_ZSHARE") == nullptr &&
+        2 * size_t(F) * ldz * sizeof(T) <= ZSHARE_MAX_BYTES) {
+      CK(cudaMalloc(&Zgn, size_t(F) * ldz * sizeof(T)));
+      CK(cudaMalloc(&Zgd, size_t(F) * ldz * sizeof(T)));
+    }
     return 0;
   }
 
@@ -464,8 +479,10 @@ struct Engine : EngineBase {
     size_t sm = smem_wside();
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
     dim3 grid((F + ST_TF - 1) / ST_TF, S);
+    T* zn = (zs_use == 1 && MODE == PM_UPDATE) ? Zgn : nullptr;
+    T* zd = (zn && bc != BC_1) ? Zgd : nullptr;
     kern<<<grid, ST_THREADS, sm, stream>>>(V, ldv, F, N, K, Wp, Hp, C1, C2, seg_cols, sc,
-                                           wpart, hside_nbuf(), st, slot);
+                                           wpart, hside_nbuf(), st, slot, zn, zd, ldz);
     CK(cudaGetLastError());
     launches += 1;
     return 0;
@@ -478,6 +495,9 @@ struct Engine : EngineBase {
     size_t sm = smem_hside();
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
     const int cs = hside_cluster();
+    const T* zn = (zs_use == 2 && MODE == PM_UPDATE) ? Zgn : nullptr;
+    const T* zd = (zn && bc != BC_1) ? Zgd : nullptr;
+    size_t ldz_ = ldz;
     if (cs > 1) {
       // few column blocks (fp64): the rows of a block are split over a cluster of cs CTAs
       cudaLaunchConfig_t cfg{};
@@ -497,10 +517,11 @@ struct Engine : EngineBase {
       int nb = hside_nbuf();
       const RunState* stc = st;
       CK(cudaLaunchKernelEx(&cfg, kern, Vc, ldv, F, N, K, Wp, Hp, C1, C2, Hb, Ho, csum, den_ones,
-                            sc, hpart, nb, stc, slot));
+                            sc, hpart, nb, stc, slot, zn, zd, ldz_));
     } else {
       kern<<<n_hblocks, ST_THREADS, sm, stream>>>(V, ldv, F, N, K, Wp, Hp, C1, C2, Hb, Ho, colsum,
-                                                  den_ones, sc, hpart, hside_nbuf(), st, slot);
+                                                  den_ones, sc, hpart, hside_nbuf(), st, slot, zn,
+                                                  zd, ldz_);
     }
     CK(cudaGetLastError());
     launches += 1;
@@ -624,10 +645,18 @@ struct Engine : EngineBase {
         // (at l == 0 they are chi(H~, H~), written by scale_h_chi of the previous iteration
         // or by step() before the first one)
         if (l > 0 && (rc = chi(Hc, Ht, C1h, C2h, nk, slot))) return rc;
-        if ((rc = w_update(Wt, Ht, C1h, C2h, Wt, Wc, slot, C1w, C2w))) return rc;
+        // fp64: the W-side pass leaves Z (same anchor for both updates of a JMM iteration) in
+        // global memory for the H-side pass
+        zs_use = Zgn ? 1 : 0;
+        rc = w_update(Wt, Ht, C1h, C2h, Wt, Wc, slot, C1w, C2w);
+        zs_use = 0;
+        if (rc) return rc;
         if (den_ones && (rc = colsums(C2w, slot))) return rc;
         if (l == 0 && (rc = prof_mark(true, slot))) return rc;
-        if ((rc = hside(PM_UPDATE, Wt, Ht, C1w, C2w, Ht, Hc, den_ones, slot))) return rc;
+        zs_use = Zgn ? 2 : 0;
+        rc = hside(PM_UPDATE, Wt, Ht, C1w, C2w, Ht, Hc, den_ones, slot);
+        zs_use = 0;
+        if (rc) return rc;
         if (l == 0 && (rc = prof_mark(false, slot))) return rc;
       }
     } else {

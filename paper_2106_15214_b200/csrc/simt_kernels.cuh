@@ -158,7 +158,8 @@ wside_partials(const T* __restrict__ V, size_t ldv, int F, int N, int K,
                const T* __restrict__ Wp, const T* __restrict__ Hp,
                const T* __restrict__ C1, const T* __restrict__ C2,
                int seg_cols, Scalars sc, double* __restrict__ part, int nbuf,
-               const RunState* st, int slot) {
+               const RunState* st, int slot, T* __restrict__ zgn, T* __restrict__ zgd,
+               size_t ldz) {
   if (!iter_active(st, slot)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int ks = kstride(K);
@@ -225,6 +226,17 @@ wside_partials(const T* __restrict__ V, size_t ldv, int F, int N, int K,
         for (int r2 = 0; r2 < vn; ++r2) segs += C2b[r2 * ks + threadIdx.x];
       }
       __syncthreads();
+      // JMM: the H-side pass of this outer iteration uses the same anchor, hence the same Z
+      // (updates.py:184-200); it reads the tiles back instead of forming W~H~ and Z again
+      if (zgn) {
+        for (int e = threadIdx.x; e < ST_TF * ST_NC; e += ST_THREADS) {
+          const int f = e / ST_NC, n = e - f * ST_NC;
+          if (f0 + f < F && n0 + n < nend) {
+            zgn[(size_t)(f0 + f) * ldz + n0 + n] = Zn[f * (ST_NC + 1) + n];
+            if (zgd) zgd[(size_t)(f0 + f) * ldz + n0 + n] = Zd[f * (ST_NC + 1) + n];
+          }
+        }
+      }
 #pragma unroll 2
       for (int n4 = 0; n4 < ST_NC / 4; ++n4) {
         const double an = Zn[(8 * r + g) * (ST_NC + 1) + 4 * n4 + t];
@@ -319,7 +331,8 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
            const T* __restrict__ C1w, const T* __restrict__ C2w,
            const T* __restrict__ Hbase, T* __restrict__ Hout,
            const double* __restrict__ colsum_c2, int den_ones, Scalars sc,
-           double* __restrict__ part, int nbuf, const RunState* st, int slot) {
+           double* __restrict__ part, int nbuf, const RunState* st, int slot,
+           const T* __restrict__ zgn, const T* __restrict__ zgd, size_t ldz) {
   if (!iter_active(st, slot)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int ks = kstride(K);
@@ -359,9 +372,12 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
     double cs = 0.0;
     const int bstride = 3 * ST_TF * ks;   // doubles between the two row stages
     // rows of tile f0 into stage b, one cp.async group
+    // Z of the W-side pass of the same outer iteration (JMM, same anchor) read back from global
+    // memory instead of the model tile + Z rule; the W~ rows are then not needed
+    const bool zread = (MODE != PM_KKT) && zgn != nullptr;
     auto stage = [&](int f0, int b) {
       const int valid_f = min(ST_TF, F - f0);
-      load_rows_async(Ws + b * bstride, Wp + (size_t)f0 * K, ST_TF, valid_f, K, ks);
+      if (!zread) load_rows_async(Ws + b * bstride, Wp + (size_t)f0 * K, ST_TF, valid_f, K, ks);
       if (MODE != PM_KKT) {
         load_rows_async(C1s + b * bstride, C1w + (size_t)f0 * K, ST_TF, valid_f, K, ks);
         if (use_den || fold_cs)
@@ -389,7 +405,16 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
       const double* Wb = Ws + b * bstride;
       const double* C1b = C1s + b * bstride;
       const double* C2b = C2s + b * bstride;
-      z_tile<BC, MODE, T>(V, ldv, F, N, f0, n0, Wb, Hs, K, ks, kappa, beta, Zn, Zd);
+      if (zread) {
+        for (int e = threadIdx.x; e < ST_TF * ST_NC; e += ST_THREADS) {
+          const int f = e / ST_NC, n = e - f * ST_NC;
+          const bool ok = f0 + f < F && n0 + n < N;
+          Zn[f * (ST_NC + 1) + n] = ok ? zgn[(size_t)(f0 + f) * ldz + n0 + n] : 0.0;
+          if (use_den) Zd[f * (ST_NC + 1) + n] = ok ? zgd[(size_t)(f0 + f) * ldz + n0 + n] : 0.0;
+        }
+      } else {
+        z_tile<BC, MODE, T>(V, ldv, F, N, f0, n0, Wb, Hs, K, ks, kappa, beta, Zn, Zd);
+      }
       if (fold_cs && threadIdx.x < K) {
         const int vf = min(ST_TF, F - f0);
         for (int r = 0; r < vf; ++r) cs += C2b[r * ks + threadIdx.x];

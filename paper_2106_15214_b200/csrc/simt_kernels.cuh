@@ -375,9 +375,26 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
     // Z of the W-side pass of the same outer iteration (JMM, same anchor) read back from global
     // memory instead of the model tile + Z rule; the W~ rows are then not needed
     const bool zread = (MODE != PM_KKT) && zgn != nullptr;
+    // numerator-only case (beta = 1) with room in the unused W~ slot of the stage: the Z tile is
+    // prefetched with the stage's cp.async group, one tile ahead like the factor rows
+    const bool zpre = zread && !use_den && ks >= ST_NC + 1;
     auto stage = [&](int f0, int b) {
       const int valid_f = min(ST_TF, F - f0);
       if (!zread) load_rows_async(Ws + b * bstride, Wp + (size_t)f0 * K, ST_TF, valid_f, K, ks);
+      if (zpre) {
+        double* zt = Ws + b * bstride;
+        const unsigned z0 = static_cast<unsigned>(__cvta_generic_to_shared(zt));
+        for (int e = threadIdx.x; e < ST_TF * ST_NC; e += ST_THREADS) {
+          const int f = e / ST_NC, n = e - f * ST_NC;
+          if (f0 + f < F && n0 + n < N)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                             z0 + 8u * (f * (ST_NC + 1) + n)),
+                         "l"(zgn + (size_t)(f0 + f) * ldz + n0 + n)
+                         : "memory");
+          else
+            zt[f * (ST_NC + 1) + n] = 0.0;
+        }
+      }
       if (MODE != PM_KKT) {
         load_rows_async(C1s + b * bstride, C1w + (size_t)f0 * K, ST_TF, valid_f, K, ks);
         if (use_den || fold_cs)
@@ -405,7 +422,9 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
       const double* Wb = Ws + b * bstride;
       const double* C1b = C1s + b * bstride;
       const double* C2b = C2s + b * bstride;
-      if (zread) {
+      if (zpre) {
+        // the tile arrived with the stage
+      } else if (zread) {
         for (int e = threadIdx.x; e < ST_TF * ST_NC; e += ST_THREADS) {
           const int f = e / ST_NC, n = e - f * ST_NC;
           const bool ok = f0 + f < F && n0 + n < N;
@@ -421,9 +440,10 @@ hside_pass(const T* __restrict__ V, size_t ldv, int F, int N, int K,
       }
       __syncthreads();
       const T* A1 = (MODE == PM_KKT) ? Wb : C1b;
+      const double* Znp = zpre ? Wb : Zn;
 #pragma unroll 2
       for (int f4 = 0; f4 < ST_TF / 4; ++f4) {
-        const double bn = Zn[(4 * f4 + t) * (ST_NC + 1) + 8 * c + g];
+        const double bn = Znp[(4 * f4 + t) * (ST_NC + 1) + 8 * c + g];
         const double bd = Zd[(4 * f4 + t) * (ST_NC + 1) + 8 * c + g];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {

@@ -111,6 +111,7 @@ struct Engine : EngineBase {
   double* fstats = nullptr;   // min / max / sum / non-finite of the uploaded factors
   // schedule
   int S = 1, seg_cols = 32;
+  int S_obj = 1, seg_cols_obj = 32;   // the objective pass's own column segments
   int n_hblocks = 1, n_oblocks = 1;
   int num_sms = 148;
   bnmf_params p{};
@@ -370,7 +371,15 @@ struct Engine : EngineBase {
     seg_cols = ((N + S - 1) / S + ST_NC - 1) / ST_NC * ST_NC;
     S = (N + seg_cols - 1) / seg_cols;
     n_hblocks = ctiles;
-    n_oblocks = ftiles * S;
+    // the objective pass is lighter (64 registers, one H~ stage): finer segments in fp64
+    {
+      int cpo = std::is_same<T, double>::value ? 4 : cps;
+      if (const char* e = getenv("BNMF_OBJ_CPS")) cpo = std::max(1, atoi(e));
+      S_obj = std::max(1, std::min(ctiles, (cpo * num_sms + ftiles - 1) / ftiles));
+      seg_cols_obj = ((N + S_obj - 1) / S_obj + ST_NC - 1) / ST_NC * ST_NC;
+      S_obj = (N + seg_cols_obj - 1) / seg_cols_obj;
+    }
+    n_oblocks = ftiles * S_obj;
     CK(cudaMalloc(&wpart, size_t(S) * 2 * fk * sizeof(double)));
     CK(cudaMalloc(&comm, (2 * fk + 8) * sizeof(double)));
     CK(cudaMalloc(&opart, size_t(std::max(n_oblocks, n_hblocks)) * sizeof(double)));
@@ -533,8 +542,8 @@ struct Engine : EngineBase {
     auto kern = objective_partials<BC, T>;
     size_t sm = smem_obj();
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-    dim3 grid((F + ST_TF - 1) / ST_TF, S);
-    kern<<<grid, ST_THREADS, sm, stream>>>(V, ldv, F, N, K, W, H, seg_cols, sc, opart, st, slot);
+    dim3 grid((F + ST_TF - 1) / ST_TF, S_obj);
+    kern<<<grid, ST_THREADS, sm, stream>>>(V, ldv, F, N, K, W, H, seg_cols_obj, sc, opart, st, slot);
     CK(cudaGetLastError());
     launches += 1;
     return 0;

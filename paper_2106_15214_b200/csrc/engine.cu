@@ -595,7 +595,7 @@ struct Engine : EngineBase {
     if (int rc = wside(PM_UPDATE, Wp, Hp, C1, C2, slot)) return rc;
     if (nranks == 1) {
       // one rank: segment reduction, update and chi maps in one launch
-      reduce_update_w<T><<<grid_for(fk), 256, 0, stream>>>(wpart, 2 * fk, S, base, F, K, out, c1o,
+      reduce_update_w<T><<<grid_for(fk, 64), 64, 0, stream>>>(wpart, 2 * fk, S, base, F, K, out, c1o,
                                                           c2o, comm, sc, st, slot);
       CK(cudaGetLastError());
       launches += 1;

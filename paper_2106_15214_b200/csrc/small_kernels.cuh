@@ -80,9 +80,21 @@ __global__ void reduce_update_w(const double* __restrict__ part, size_t stride, 
   const int fk = F * K;
   const T beta = T(sc.beta);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < fk; i += gridDim.x * blockDim.x) {
+    // the segment partials are loaded in batches of 8 + 8 (independent loads in flight), then
+    // added in segment order
     double num = 0.0, den = 0.0;
-#pragma unroll 8
-    for (int k = 0; k < S; ++k) {
+    int k = 0;
+    for (; k + 8 <= S; k += 8) {
+      double a[8], b[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a[u] = part[(size_t)(k + u) * stride + i];
+        b[u] = part[(size_t)(k + u) * stride + fk + i];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { num += a[u]; den += b[u]; }
+    }
+    for (; k < S; ++k) {
       num += part[(size_t)k * stride + i];
       den += part[(size_t)k * stride + fk + i];
     }
